@@ -1,0 +1,154 @@
+/* femgpu -- B200-native finite element local assembly (sm_100a, FP64).
+ *
+ * Drop-in replacement for the per-element kernels the reference (femopt,
+ * arXiv 1604.05872) emits as C.  Library conventions mirror libfemopt
+ * (/root/reference/proj/include/femopt.h:1-76):
+ *   - opaque handle (femopt_kernel, femopt.h:18)  ->  femgpu_form;
+ *   - every function returns 0 on success or an error code, femopt's codes
+ *     1-11 keep their meaning (femopt.h:20-33) and 12-14 add device errors;
+ *   - the message of the most recent failure on the calling thread is
+ *     femgpu_last_error() (femopt_last_error, femopt.h:72-74;
+ *     thread_local in capi.cpp:13);
+ *   - no C++ exception ever crosses this ABI (capi.cpp:33-46, `guarded`).
+ * Handles are reentrant: distinct forms may be used concurrently, one form may
+ * be used from several threads on distinct streams.
+ *
+ * Data layout (all FP64, cell-major, row-major inside a cell):
+ *   coords [E][4][3]   vertex coordinates of each tetrahedron
+ *   coeffs [E][ncoef]  coefficient dofs, per form (see femgpu_form_kind)
+ *   A      [E][n][n]   element matrix (component-blocked for vector forms)
+ */
+#ifndef FEMGPU_H
+#define FEMGPU_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct femgpu_form femgpu_form;
+
+typedef enum femgpu_error {
+  FEMGPU_OK = 0,
+  FEMGPU_ERR_PARSE = 1,              /* femopt.h:22 (unused here)            */
+  FEMGPU_ERR_UNKNOWN_LOOP = 2,       /* femopt.h:23 (unused here)            */
+  FEMGPU_ERR_NOT_FEM_NEST = 3,       /* femopt.h:24: unsupported form shape  */
+  FEMGPU_ERR_NON_DISTRIBUTABLE = 4,  /* femopt.h:25 (unused here)            */
+  FEMGPU_ERR_NON_SEPARABLE = 5,      /* femopt.h:26 (unused here)            */
+  FEMGPU_ERR_NOT_NORMAL_FORM = 6,    /* femopt.h:27 (unused here)            */
+  FEMGPU_ERR_TOO_MANY_MONOMIALS = 7, /* femopt.h:28 (unused here)            */
+  FEMGPU_ERR_INCONSISTENT_LAYOUT = 8,/* femopt.h:29: table shapes disagree   */
+  FEMGPU_ERR_INVALID_ARG = 9,        /* femopt.h:30                          */
+  FEMGPU_ERR_IO = 10,                /* femopt.h:31 (unused here)            */
+  FEMGPU_ERR_INTERNAL = 11,          /* femopt.h:32                          */
+  FEMGPU_ERR_CUDA = 12,              /* a CUDA runtime call failed           */
+  FEMGPU_ERR_NO_DEVICE = 13,         /* no sm_100 device / kernel image      */
+  FEMGPU_ERR_UNSUPPORTED = 14        /* valid form, no kernel for its size   */
+} femgpu_error;
+
+/* Forms (BASELINE.json configs).  `ncoef` is the per-cell coefficient width.
+ *   HELMHOLTZ        a(u,v) = int f (grad u . grad v + u v)
+ *                    scalar P_k (k = degree), f in P_{coef_degree}:
+ *                    coeffs = f dofs [nc]
+ *   ELASTICITY       a(u,v) = int 2 mu eps(u):eps(v) + lam div u div v
+ *                    vector P_k, mu, lam in P1: coeffs = [mu(4), lam(4)]
+ *   HYPERELASTICITY  St Venant-Kirchhoff tangent at displacement w:
+ *                    int (grad du S + F dS[du]) : grad v,  F = I + grad w
+ *                    coeffs = [w (3 x ns, component-blocked), mu(4), lam(4)]
+ *   BURGERS          int du.v/dt + (du.grad)u.v + (u.grad)du.v + nu grad du:grad v
+ *                    coeffs = u (3 x ns, component-blocked); consts = {nu, dt}
+ */
+typedef enum femgpu_form_kind {
+  FEMGPU_HELMHOLTZ = 1,
+  FEMGPU_ELASTICITY = 2,
+  FEMGPU_HYPERELASTICITY = 3,
+  FEMGPU_BURGERS = 4
+} femgpu_form_kind;
+
+/* Kernel schedules (the paper's two strategies, §3.2-3.3):
+ *   TENSOR      pre-evaluated reference tensors contracted with per-cell
+ *               geometry/coefficient factors (preeval.cpp:279-451)
+ *   QUADRATURE  per-quadrature-point sharing-eliminated accumulation
+ *               (sharing.cpp:409-607)
+ * AUTO picks the schedule this library measured fastest for the form. */
+typedef enum femgpu_schedule {
+  FEMGPU_SCHED_AUTO = 0,
+  FEMGPU_SCHED_TENSOR = 1,
+  FEMGPU_SCHED_QUADRATURE = 2
+} femgpu_schedule;
+
+/* Reference tables of a form: exactly the input tables femopt's IR carries
+ * (paper_1604_05872_b200/ir.py), on the reference tetrahedron
+ * (0,0,0),(1,0,0),(0,1,0),(0,0,1).  Host pointers; copied at create time. */
+typedef struct femgpu_form_desc {
+  int kind;             /* femgpu_form_kind */
+  int nq;               /* quadrature points Q */
+  int ns;               /* scalar basis functions per component */
+  int nc;               /* coefficient basis functions (cols of P) */
+  const double* W;      /* [Q] weights */
+  const double* B;      /* [Q][ns] basis values */
+  const double* D;      /* [3][Q][ns] reference gradients d/dX_a */
+  const double* P;      /* [Q][nc] coefficient basis values */
+  double consts[4];     /* BURGERS: {nu, dt}; others ignored */
+  int schedule;         /* femgpu_schedule */
+} femgpu_form_desc;
+
+typedef struct femgpu_form_info {
+  int n;                      /* element matrix is n x n */
+  int ncoef;                  /* coefficient dofs per cell */
+  int schedule;               /* schedule in use */
+  double flops_per_cell;      /* FP64 flops the chosen kernels execute per cell */
+  double bytes_per_cell;      /* compulsory HBM bytes: 8*(12 + ncoef + n*n) */
+  int kernels_per_launch;     /* device kernels one femgpu_assemble launches */
+  char kernel_name[64];       /* dominant kernel's name */
+} femgpu_form_info;
+
+/* Creates a form on the current CUDA device: validates the tables, computes
+ * the schedule's pre-evaluated reference tensors on the host in FP64
+ * (ascending-quadrature-point left folds, as preeval.cpp:269-274), and uploads
+ * them.  *out must be released with femgpu_form_free(). */
+int femgpu_form_create(const femgpu_form_desc* desc, femgpu_form** out);
+void femgpu_form_free(femgpu_form* f);
+int femgpu_form_get_info(const femgpu_form* f, femgpu_form_info* info);
+
+/* Element matrices of cells [0, ncells) -- the hot path.  Device pointers
+ * (cell-major layout above), stream = cudaStream_t (NULL = legacy default).
+ * accumulate = 0 overwrites A; nonzero adds into it (the emitted-C `+=`
+ * contract, emit_c.cpp:129).  Asynchronous: returns after enqueueing. */
+int femgpu_assemble(const femgpu_form* f, long ncells, const double* coords,
+                    const double* coeffs, double* A, int accumulate, void* stream);
+
+/* Same, from and to HOST memory: copies in, assembles and copies out in a
+ * chunked multi-stream pipeline (the end-to-end path).  Synchronous.
+ * Pinned host buffers give full PCIe bandwidth; pageable ones work too. */
+int femgpu_assemble_host(const femgpu_form* f, long ncells, const double* coords,
+                         const double* coeffs, double* A, int accumulate);
+
+/* The emitted-C element-kernel interface (emit_c.cpp:127-141) through the
+ * reference harness's uniform entry point (test_backend.cpp:62-73):
+ *   o = outputs in name order, t = input tables in name order, c = constants,
+ * with femopt's IR naming for this form (paper_1604_05872_b200/ir.py) and
+ * HOST pointers.  Per-cell tables are the SoA e-tables (x{v}{c}[e], dofs);
+ * reference tables (W, B, D*, P*) are accepted and ignored in favour of the
+ * form's own copies.  Outputs are accumulated with `+=` like emitted C.
+ * `ncells` replaces the literal E of the emitted code. */
+int femgpu_kernel_argv(const femgpu_form* f, long ncells, double* const* o,
+                       const double* const* t, const double* c);
+
+/* Number and names of the arguments femgpu_kernel_argv expects, in order
+ * (group: 0 = output, 1 = table, 2 = constant). */
+int femgpu_kernel_argc(const femgpu_form* f, int group, int* count);
+int femgpu_kernel_argname(const femgpu_form* f, int group, int index, char* buf, size_t len);
+
+/* Message for the most recent failure on this thread ("" if none). */
+const char* femgpu_last_error(void);
+
+/* Library build string (arch, version). */
+const char* femgpu_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FEMGPU_H */

@@ -1,0 +1,552 @@
+// capi.cu -- the femgpu C ABI (include/femgpu.h): form handles, host-side
+// pre-evaluation of reference tensors, dispatch to the sm_100a kernels,
+// the host-memory end-to-end pipeline and the emitted-C argv entry point.
+//
+// Conventions follow libfemopt (proj/src/capi.cpp): thread-local last error
+// (:13), exceptions caught at the boundary and mapped to int codes (:15-46).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/femgpu.h"
+#include "femgpu_internal.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    int code = (e == cudaErrorNoDevice || e == cudaErrorNoKernelImageForDevice ||
+                e == cudaErrorInsufficientDriver)
+                   ? FEMGPU_ERR_NO_DEVICE
+                   : FEMGPU_ERR_CUDA;
+    throw Error(code, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+  try {
+    fn();
+    g_last_error.clear();
+    return FEMGPU_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "out of host memory";
+    return FEMGPU_ERR_INTERNAL;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return FEMGPU_ERR_INTERNAL;
+  }
+}
+
+enum Route { ROUTE_HELM_P1, ROUTE_HELM_TENSOR, ROUTE_PAIR, ROUTE_BURGERS };
+
+std::string two(int m) {
+  char b[8];
+  std::snprintf(b, sizeof b, "%02d", m);
+  return b;
+}
+
+}  // namespace
+
+struct femgpu_form {
+  int kind = 0, nq = 0, ns = 0, nc = 0, n = 0, ncoef = 0;
+  int schedule = 0, route = 0, device = 0;
+  double consts[4] = {0, 0, 0, 0};
+  std::vector<double> W, B, D, P;
+  femgpu::HelmP1Params p1{};
+  double* d_tab = nullptr;
+  size_t tab_doubles = 0;
+  double flops_per_cell = 0;
+  int kernels_per_launch = 1;
+  std::string kernel_name;
+  std::vector<std::string> argv_out, argv_tab, argv_con;
+
+  ~femgpu_form() {
+    if (d_tab) {
+      int cur = 0;
+      cudaGetDevice(&cur);
+      cudaSetDevice(device);
+      cudaFree(d_tab);
+      cudaSetDevice(cur);
+    }
+  }
+};
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// Host pre-evaluation (the reference's symbolic_reduce, preeval.cpp:190-277:
+// tables summed over the reduction index in ascending order).
+// ---------------------------------------------------------------------------
+
+double Dv(const femgpu_form* f, int a, int q, int j) {
+  return f->D[((size_t)a * f->nq + q) * f->ns + j];
+}
+
+void build_helm_p1(femgpu_form* f) {
+  auto& p = f->p1;
+  std::memset(&p, 0, sizeof p);
+  for (int m = 0; m < f->nc; ++m) {
+    double s = 0.0;
+    for (int q = 0; q < f->nq; ++q) s += f->W[q] * f->P[(size_t)q * f->nc + m];
+    p.c[m] = s;
+    int pp = 0;
+    for (int j = 0; j < 4; ++j)
+      for (int k = j; k < 4; ++k, ++pp) {
+        double t = 0.0;
+        for (int q = 0; q < f->nq; ++q)
+          t += f->W[q] * f->P[(size_t)q * f->nc + m] * f->B[(size_t)q * 4 + j] * f->B[(size_t)q * 4 + k];
+        p.M[m][pp] = t;
+      }
+  }
+  for (int j = 0; j < 4; ++j)
+    for (int a = 0; a < 3; ++a) p.Dr[j][a] = Dv(f, a, 0, j);
+  // stiffness 10 pairs x (3 mul+2 add) + geometry ~60 + gradients 36*2 + mass/combine
+  f->flops_per_cell = 60 + 72 + 8 + 10 * (5 + 8 + 3);
+  f->kernel_name = "helm_p1_kernel";
+}
+
+void build_helm_tensor(femgpu_form* f, std::vector<double>& host) {
+  int KS, NT, KR, NP;
+  femgpu::helm_tensor_geometry(f->ns, f->nc, &KS, &NT, &KR, &NP);
+  const int ns = f->ns, nc = f->nc, Q = f->nq;
+  // S[alpha = m*7+s][p = (j<=k)]
+  std::vector<double> S((size_t)KR * NP, 0.0);
+  const int ab[6][2] = {{0, 0}, {1, 1}, {2, 2}, {0, 1}, {0, 2}, {1, 2}};
+  std::vector<double> wp(Q);
+  for (int m = 0; m < nc; ++m) {
+    for (int q = 0; q < Q; ++q) wp[q] = f->W[q] * f->P[(size_t)q * nc + m];
+    int p = 0;
+    for (int j = 0; j < ns; ++j)
+      for (int k = j; k < ns; ++k, ++p) {
+        for (int s = 0; s < 7; ++s) {
+          double acc = 0.0;
+          for (int q = 0; q < Q; ++q) {
+            double v;
+            if (s == 6) {
+              v = f->B[(size_t)q * ns + j] * f->B[(size_t)q * ns + k];
+            } else {
+              const int a = ab[s][0], b = ab[s][1];
+              v = Dv(f, a, q, j) * Dv(f, b, q, k);
+              if (a != b) v += Dv(f, b, q, j) * Dv(f, a, q, k);
+            }
+            acc += wp[q] * v;
+          }
+          S[(size_t)(m * 7 + s) * NP + p] = acc;
+        }
+      }
+  }
+  host.assign((size_t)KS * NT * 64, 0.0);
+  for (int ks = 0; ks < KS; ++ks)
+    for (int nt = 0; nt < NT; ++nt)
+      for (int lane = 0; lane < 32; ++lane)
+        for (int v = 0; v < 2; ++v) {
+          const int g = lane >> 2, t = lane & 3;
+          const int k = ks * 8 + t + 4 * v, n = nt * 8 + g;
+          host[((size_t)(ks * NT + nt) * 32 + lane) * 2 + v] =
+              (k < KR && n < NP) ? S[(size_t)k * NP + n] : 0.0;
+        }
+  f->flops_per_cell = 2.0 * KR * NP + 60 + 36 + KR;
+  f->kernel_name = "helm_tensor_kernel";
+}
+
+void build_argv_names(femgpu_form* f) {
+  auto& T = f->argv_tab;
+  T.clear();
+  f->argv_out.clear();
+  f->argv_con.clear();
+  for (int v = 0; v < 4; ++v)
+    for (int c = 0; c < 3; ++c) T.push_back("x" + std::to_string(v) + std::to_string(c));
+  T.push_back("W");
+  const int ns = f->ns;
+  switch (f->kind) {
+    case FEMGPU_HELMHOLTZ:
+      T.push_back("B");
+      for (int a = 0; a < 3; ++a) T.push_back("D" + std::to_string(a));
+      for (int m = 0; m < f->nc; ++m) {
+        T.push_back("P" + two(m));
+        T.push_back("f" + two(m));
+      }
+      f->argv_out.push_back("A");
+      break;
+    case FEMGPU_ELASTICITY:
+    case FEMGPU_HYPERELASTICITY:
+      for (int c = 0; c < 3; ++c)
+        for (int a = 0; a < 3; ++a) T.push_back("Dv" + std::to_string(c) + std::to_string(a));
+      for (int m = 0; m < 4; ++m) {
+        T.push_back("P" + std::to_string(m));
+        T.push_back("mu" + std::to_string(m));
+        T.push_back("lam" + std::to_string(m));
+      }
+      if (f->kind == FEMGPU_HYPERELASTICITY)
+        for (int m = 0; m < ns; ++m)
+          for (int a = 0; a < 3; ++a) {
+            T.push_back("Dw" + std::to_string(a) + two(m));
+            T.push_back("w" + std::to_string(a) + two(m));
+          }
+      f->argv_out.push_back("A");
+      break;
+    case FEMGPU_BURGERS:
+      T.push_back("B");
+      for (int a = 0; a < 3; ++a) T.push_back("D" + std::to_string(a));
+      for (int m = 0; m < ns; ++m) {
+        T.push_back("P" + two(m));
+        for (int a = 0; a < 3; ++a) {
+          T.push_back("Du" + std::to_string(a) + two(m));
+          T.push_back("u" + std::to_string(a) + two(m));
+        }
+      }
+      for (int c = 0; c < 3; ++c)
+        for (int d = 0; d < 3; ++d) f->argv_out.push_back("A" + std::to_string(c) + std::to_string(d));
+      f->argv_con = {"dt", "nu"};
+      break;
+  }
+  std::sort(T.begin(), T.end());
+  std::sort(f->argv_out.begin(), f->argv_out.end());
+  std::sort(f->argv_con.begin(), f->argv_con.end());
+}
+
+// Column of cell-major coeffs that IR e-table `name` maps to, or -1.
+int coef_column(const femgpu_form* f, const std::string& name) {
+  const int ns = f->ns;
+  auto num = [&](size_t from) { return std::atoi(name.c_str() + from); };
+  switch (f->kind) {
+    case FEMGPU_HELMHOLTZ:
+      if (name.size() == 3 && name[0] == 'f') return num(1);
+      break;
+    case FEMGPU_ELASTICITY:
+      if (name.rfind("mu", 0) == 0) return num(2);
+      if (name.rfind("lam", 0) == 0) return 4 + num(3);
+      break;
+    case FEMGPU_HYPERELASTICITY:
+      if (name.rfind("mu", 0) == 0) return 3 * ns + num(2);
+      if (name.rfind("lam", 0) == 0) return 3 * ns + 4 + num(3);
+      if (name[0] == 'w' && name.size() == 4) return (name[1] - '0') * ns + num(2);
+      break;
+    case FEMGPU_BURGERS:
+      if (name[0] == 'u' && name.size() == 4) return (name[1] - '0') * ns + num(2);
+      break;
+  }
+  return -1;
+}
+
+void validate(const femgpu_form_desc* d) {
+  if (!d) throw Error(FEMGPU_ERR_INVALID_ARG, "null form descriptor");
+  if (d->kind < FEMGPU_HELMHOLTZ || d->kind > FEMGPU_BURGERS)
+    throw Error(FEMGPU_ERR_INVALID_ARG, "unknown form kind " + std::to_string(d->kind));
+  if (d->nq <= 0 || d->ns <= 0 || d->nc < 0)
+    throw Error(FEMGPU_ERR_INCONSISTENT_LAYOUT, "non-positive table extent");
+  if (!d->W || !d->B || !d->D || (d->nc > 0 && !d->P))
+    throw Error(FEMGPU_ERR_INVALID_ARG, "null reference table");
+  if ((d->kind == FEMGPU_ELASTICITY || d->kind == FEMGPU_HYPERELASTICITY) && d->nc != 4)
+    throw Error(FEMGPU_ERR_INCONSISTENT_LAYOUT, "mu and lambda must be P1 (nc == 4)");
+  if (d->kind == FEMGPU_BURGERS && !(d->consts[1] != 0.0))
+    throw Error(FEMGPU_ERR_INVALID_ARG, "Burgers needs dt != 0 (consts[1])");
+  if (d->schedule < FEMGPU_SCHED_AUTO || d->schedule > FEMGPU_SCHED_QUADRATURE)
+    throw Error(FEMGPU_ERR_INVALID_ARG, "unknown schedule");
+}
+
+bool constant_gradients(const femgpu_form* f) {
+  for (int a = 0; a < 3; ++a)
+    for (int q = 1; q < f->nq; ++q)
+      for (int j = 0; j < f->ns; ++j)
+        if (Dv(f, a, q, j) != Dv(f, a, 0, j)) return false;
+  return true;
+}
+
+void check_ptr(const void* p, const char* what) {
+  if (!p) throw Error(FEMGPU_ERR_INVALID_ARG, std::string("null ") + what);
+  if (reinterpret_cast<uintptr_t>(p) % 16 != 0)
+    throw Error(FEMGPU_ERR_INVALID_ARG, std::string(what) + " must be 16-byte aligned");
+}
+
+void launch(const femgpu_form* f, long E, const double* coords, const double* coef, double* A,
+            int acc, cudaStream_t s) {
+  cudaError_t e = cudaSuccess;
+  switch (f->route) {
+    case ROUTE_HELM_P1:
+      e = femgpu::launch_helm_p1(f->p1, E, coords, coef, A, acc, s);
+      break;
+    case ROUTE_HELM_TENSOR:
+      e = femgpu::launch_helm_tensor(f->ns, f->nc, E, coords, coef, f->d_tab, A, acc, s);
+      break;
+    case ROUTE_PAIR:
+      e = femgpu::launch_pair(f->kind, f->nq, f->ns, E, coords, coef, f->d_tab, A, acc, s);
+      break;
+    case ROUTE_BURGERS:
+      e = femgpu::launch_burgers(f->ns, E, coords, coef, f->d_tab, f->consts[0], f->consts[1], A,
+                                 acc, s);
+      break;
+  }
+  cuda_check(e, f->kernel_name.c_str());
+}
+
+}  // namespace
+
+extern "C" {
+
+int femgpu_form_create(const femgpu_form_desc* d, femgpu_form** out) {
+  if (!out) {
+    g_last_error = "null output handle";
+    return FEMGPU_ERR_INVALID_ARG;
+  }
+  *out = nullptr;
+  return guarded([&] {
+    validate(d);
+    auto f = std::make_unique<femgpu_form>();
+    f->kind = d->kind;
+    f->nq = d->nq;
+    f->ns = d->ns;
+    f->nc = d->nc;
+    f->n = d->kind == FEMGPU_HELMHOLTZ ? d->ns : 3 * d->ns;
+    f->ncoef = d->kind == FEMGPU_HELMHOLTZ      ? d->nc
+               : d->kind == FEMGPU_ELASTICITY   ? 8
+               : d->kind == FEMGPU_HYPERELASTICITY ? 3 * d->ns + 8
+                                               : 3 * d->ns;
+    std::memcpy(f->consts, d->consts, sizeof f->consts);
+    f->W.assign(d->W, d->W + d->nq);
+    f->B.assign(d->B, d->B + (size_t)d->nq * d->ns);
+    f->D.assign(d->D, d->D + (size_t)3 * d->nq * d->ns);
+    if (d->nc > 0) f->P.assign(d->P, d->P + (size_t)d->nq * d->nc);
+    cuda_check(cudaGetDevice(&f->device), "cudaGetDevice");
+    std::vector<double> host;
+    switch (d->kind) {
+      case FEMGPU_HELMHOLTZ:
+        if (d->ns == 4 && d->nc <= 4 && constant_gradients(f.get()) &&
+            d->schedule != FEMGPU_SCHED_QUADRATURE) {
+          f->route = ROUTE_HELM_P1;
+          build_helm_p1(f.get());
+        } else if (femgpu::helm_tensor_supported(d->ns, d->nc) &&
+                   d->schedule != FEMGPU_SCHED_QUADRATURE) {
+          f->route = ROUTE_HELM_TENSOR;
+          build_helm_tensor(f.get(), host);
+        } else {
+          throw Error(FEMGPU_ERR_UNSUPPORTED, "no Helmholtz kernel for ns=" +
+                                                  std::to_string(d->ns) + " nc=" + std::to_string(d->nc));
+        }
+        f->schedule = FEMGPU_SCHED_TENSOR;
+        break;
+      case FEMGPU_ELASTICITY:
+      case FEMGPU_HYPERELASTICITY: {
+        if (!femgpu::pair_supported(d->kind, d->nq, d->ns) || d->schedule == FEMGPU_SCHED_TENSOR)
+          throw Error(FEMGPU_ERR_UNSUPPORTED, "no vector-form kernel for this size/schedule");
+        f->route = ROUTE_PAIR;
+        f->schedule = FEMGPU_SCHED_QUADRATURE;
+        host.insert(host.end(), f->W.begin(), f->W.end());
+        host.insert(host.end(), f->D.begin(), f->D.end());
+        host.insert(host.end(), f->P.begin(), f->P.end());
+        const int npair = f->ns * (f->ns + 1) / 2;
+        const double per_q = d->kind == FEMGPU_ELASTICITY ? 24.0 : 40.0;
+        f->flops_per_cell = 60 + f->nq * (f->ns * 3 * 5 + 16 + npair * per_q * 2);
+        f->kernel_name = d->kind == FEMGPU_ELASTICITY ? "pair_kernel<elasticity>" : "pair_kernel<svk>";
+        break;
+      }
+      case FEMGPU_BURGERS:
+        if (!femgpu::burgers_supported(d->nq, d->ns) || d->schedule == FEMGPU_SCHED_QUADRATURE)
+          throw Error(FEMGPU_ERR_UNSUPPORTED, "no Burgers kernel for this size/schedule");
+        f->route = ROUTE_BURGERS;
+        f->schedule = FEMGPU_SCHED_TENSOR;
+        throw Error(FEMGPU_ERR_UNSUPPORTED, "Burgers kernel not built yet");
+    }
+    if (!host.empty()) {
+      f->tab_doubles = host.size();
+      cuda_check(cudaMalloc(&f->d_tab, host.size() * sizeof(double)), "cudaMalloc(tables)");
+      cuda_check(cudaMemcpy(f->d_tab, host.data(), host.size() * sizeof(double),
+                            cudaMemcpyHostToDevice),
+                 "cudaMemcpy(tables)");
+    }
+    build_argv_names(f.get());
+    *out = f.release();
+  });
+}
+
+void femgpu_form_free(femgpu_form* f) { delete f; }
+
+int femgpu_form_get_info(const femgpu_form* f, femgpu_form_info* info) {
+  if (!f || !info) {
+    g_last_error = "null argument";
+    return FEMGPU_ERR_INVALID_ARG;
+  }
+  return guarded([&] {
+    std::memset(info, 0, sizeof *info);
+    info->n = f->n;
+    info->ncoef = f->ncoef;
+    info->schedule = f->schedule;
+    info->flops_per_cell = f->flops_per_cell;
+    info->bytes_per_cell = 8.0 * (12 + f->ncoef + (double)f->n * f->n);
+    info->kernels_per_launch = f->kernels_per_launch;
+    std::snprintf(info->kernel_name, sizeof info->kernel_name, "%s", f->kernel_name.c_str());
+  });
+}
+
+int femgpu_assemble(const femgpu_form* f, long ncells, const double* coords, const double* coeffs,
+                    double* A, int accumulate, void* stream) {
+  if (!f) {
+    g_last_error = "null form";
+    return FEMGPU_ERR_INVALID_ARG;
+  }
+  return guarded([&] {
+    if (ncells < 0) throw Error(FEMGPU_ERR_INVALID_ARG, "negative cell count");
+    if (ncells == 0) return;
+    check_ptr(coords, "coords");
+    check_ptr(A, "A");
+    if (f->ncoef > 0) check_ptr(coeffs, "coeffs");
+    launch(f, ncells, coords, coeffs, A, accumulate, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int femgpu_assemble_host(const femgpu_form* f, long ncells, const double* coords,
+                         const double* coeffs, double* A, int accumulate) {
+  if (!f) {
+    g_last_error = "null form";
+    return FEMGPU_ERR_INVALID_ARG;
+  }
+  return guarded([&] {
+    if (ncells < 0) throw Error(FEMGPU_ERR_INVALID_ARG, "negative cell count");
+    if (ncells == 0) return;
+    if (!coords || !A || (f->ncoef > 0 && !coeffs)) throw Error(FEMGPU_ERR_INVALID_ARG, "null buffer");
+    const size_t nn = (size_t)f->n * f->n;
+    // ~64 MiB of element matrices per chunk, multiple of 64 cells
+    long chunk = std::max<long>(64, (long)((64u << 20) / (nn * 8)) / 64 * 64);
+    chunk = std::min(chunk, ncells);
+    const int NSTREAM = 3;
+    cudaStream_t st[NSTREAM];
+    double* dbuf[NSTREAM] = {nullptr, nullptr, nullptr};
+    const size_t per_cell = 12 + f->ncoef + nn;
+    struct Cleanup {
+      cudaStream_t* st;
+      double** buf;
+      int n;
+      ~Cleanup() {
+        for (int i = 0; i < n; ++i) {
+          if (buf[i]) cudaFree(buf[i]);
+          if (st[i]) cudaStreamDestroy(st[i]);
+        }
+      }
+    } cleanup{st, dbuf, NSTREAM};
+    for (int i = 0; i < NSTREAM; ++i) st[i] = nullptr;
+    for (int i = 0; i < NSTREAM; ++i) {
+      cuda_check(cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking), "cudaStreamCreate");
+      cuda_check(cudaMalloc(&dbuf[i], per_cell * chunk * sizeof(double)), "cudaMalloc(chunk)");
+    }
+    long ci = 0;
+    for (long c0 = 0; c0 < ncells; c0 += chunk, ++ci) {
+      const long E = std::min(chunk, ncells - c0);
+      const int s = (int)(ci % NSTREAM);
+      double* dx = dbuf[s];
+      double* dA = dx + 12 * chunk;  // 16B aligned: chunk is a multiple of 64
+      double* dc = dA + nn * chunk;
+      cuda_check(cudaMemcpyAsync(dx, coords + c0 * 12, E * 12 * sizeof(double),
+                                 cudaMemcpyHostToDevice, st[s]), "H2D coords");
+      if (f->ncoef > 0)
+        cuda_check(cudaMemcpyAsync(dc, coeffs + c0 * f->ncoef, E * f->ncoef * sizeof(double),
+                                   cudaMemcpyHostToDevice, st[s]), "H2D coeffs");
+      if (accumulate)
+        cuda_check(cudaMemcpyAsync(dA, A + c0 * nn, E * nn * sizeof(double),
+                                   cudaMemcpyHostToDevice, st[s]), "H2D A");
+      launch(f, E, dx, dc, dA, accumulate, st[s]);
+      cuda_check(cudaMemcpyAsync(A + c0 * nn, dA, E * nn * sizeof(double), cudaMemcpyDeviceToHost,
+                                 st[s]), "D2H A");
+    }
+    for (int i = 0; i < NSTREAM; ++i) cuda_check(cudaStreamSynchronize(st[i]), "sync");
+  });
+}
+
+int femgpu_kernel_argc(const femgpu_form* f, int group, int* count) {
+  if (!f || !count || group < 0 || group > 2) {
+    g_last_error = "bad argument";
+    return FEMGPU_ERR_INVALID_ARG;
+  }
+  *count = (int)(group == 0 ? f->argv_out.size() : group == 1 ? f->argv_tab.size() : f->argv_con.size());
+  g_last_error.clear();
+  return FEMGPU_OK;
+}
+
+int femgpu_kernel_argname(const femgpu_form* f, int group, int index, char* buf, size_t len) {
+  if (!f || !buf || group < 0 || group > 2) {
+    g_last_error = "bad argument";
+    return FEMGPU_ERR_INVALID_ARG;
+  }
+  const auto& v = group == 0 ? f->argv_out : group == 1 ? f->argv_tab : f->argv_con;
+  if (index < 0 || index >= (int)v.size()) {
+    g_last_error = "argument index out of range";
+    return FEMGPU_ERR_INVALID_ARG;
+  }
+  std::snprintf(buf, len, "%s", v[index].c_str());
+  g_last_error.clear();
+  return FEMGPU_OK;
+}
+
+int femgpu_kernel_argv(const femgpu_form* f, long ncells, double* const* o, const double* const* t,
+                       const double* c) {
+  if (!f || !o || !t) {
+    g_last_error = "null argument";
+    return FEMGPU_ERR_INVALID_ARG;
+  }
+  return guarded([&] {
+    if (ncells <= 0) return;
+    const long E = ncells;
+    const int ns = f->ns;
+    // SoA e-tables -> cell-major (the layout the kernels stream)
+    std::vector<double> coords((size_t)E * 12), coef((size_t)E * std::max(f->ncoef, 1));
+    for (size_t i = 0; i < f->argv_tab.size(); ++i) {
+      const std::string& name = f->argv_tab[i];
+      if (name.size() == 3 && name[0] == 'x') {
+        const int v = name[1] - '0', cc = name[2] - '0';
+        if (!t[i]) throw Error(FEMGPU_ERR_INVALID_ARG, "null table " + name);
+        for (long e = 0; e < E; ++e) coords[e * 12 + v * 3 + cc] = t[i][e];
+        continue;
+      }
+      const int col = coef_column(f, name);
+      if (col >= 0) {
+        if (!t[i]) throw Error(FEMGPU_ERR_INVALID_ARG, "null table " + name);
+        for (long e = 0; e < E; ++e) coef[e * f->ncoef + col] = t[i][e];
+      }
+    }
+    if (f->kind == FEMGPU_BURGERS && c) {
+      // constants in name order: dt, nu -- must match the form's
+      if (c[0] != f->consts[1] || c[1] != f->consts[0])
+        throw Error(FEMGPU_ERR_INCONSISTENT_LAYOUT, "constants differ from the form's (nu, dt)");
+    }
+    const size_t nn = (size_t)f->n * f->n;
+    std::vector<double> A((size_t)E * nn, 0.0);
+    int rc = femgpu_assemble_host(f, E, coords.data(), coef.data(), A.data(), 0);
+    if (rc != FEMGPU_OK) throw Error(rc, g_last_error);
+    if (f->kind == FEMGPU_BURGERS) {
+      for (int cc = 0; cc < 3; ++cc)
+        for (int d = 0; d < 3; ++d) {
+          double* out = o[cc * 3 + d];  // names A00..A22 sorted
+          for (long e = 0; e < E; ++e)
+            for (int j = 0; j < ns; ++j)
+              for (int k = 0; k < ns; ++k)
+                out[(e * ns + j) * ns + k] += A[e * nn + (size_t)(cc * ns + j) * f->n + d * ns + k];
+        }
+    } else {
+      for (size_t i = 0; i < A.size(); ++i) o[0][i] += A[i];
+    }
+  });
+}
+
+const char* femgpu_last_error(void) { return g_last_error.c_str(); }
+
+const char* femgpu_version(void) { return "femgpu 0.1 (sm_100a, FP64)"; }
+
+}  // extern "C"

@@ -1,0 +1,40 @@
+// femgpu_internal.h -- declarations shared by the host C ABI and the kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace femgpu {
+
+// Pre-evaluated P1 Helmholtz tables (kernel parameters: constant bank).
+struct HelmP1Params {
+  double c[4];      // c_m = sum_q W_q P_m(q)
+  double M[4][10];  // M_m,(j<=k) = sum_q W_q P_m(q) B_j(q) B_k(q)
+  double Dr[4][3];  // constant reference gradients, Dr[j][a] = D[a][*][j]
+};
+
+cudaError_t launch_helm_p1(const HelmP1Params& prm, long E, const double* coords,
+                           const double* coef, double* A, int acc, cudaStream_t s);
+
+bool helm_tensor_supported(int ns, int nc);
+void helm_tensor_geometry(int ns, int nc, int* KS, int* NT, int* KR, int* NP);
+cudaError_t launch_helm_tensor(int ns, int nc, long E, const double* coords, const double* coef,
+                               const double* Sfrag, double* A, int acc, cudaStream_t s);
+
+// Vector forms on CUDA cores: per-(j<=k) pair accumulation over quadrature
+// points (elasticity, St Venant-Kirchhoff).  tab = [W(Q) | D(3,Q,ns) | P(Q,4)].
+struct PairParams {
+  int kind;  // FEMGPU_ELASTICITY or FEMGPU_HYPERELASTICITY
+  int nq;
+};
+bool pair_supported(int kind, int nq, int ns);
+cudaError_t launch_pair(int kind, int nq, int ns, long E, const double* coords,
+                        const double* coef, const double* tab, double* A, int acc,
+                        cudaStream_t s);
+
+// Burgers tensor schedule (see burgers.cu).
+bool burgers_supported(int nq, int ns);
+cudaError_t launch_burgers(int ns, long E, const double* coords, const double* coef,
+                           const double* tab, double nu, double dt, double* A, int acc,
+                           cudaStream_t s);
+
+}  // namespace femgpu

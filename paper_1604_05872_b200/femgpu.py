@@ -1,0 +1,212 @@
+"""Host mirror of the femgpu C ABI (include/femgpu.h) -- ctypes, no torch types.
+
+This is the Python face of the drop-in boundary.  It mirrors the reference's
+two interfaces for the element-kernel path:
+
+* libfemopt's library conventions (/root/reference/proj/include/femopt.h):
+  int return codes 0..11 with femopt's meanings, a thread-local last-error
+  message, handle objects that own native state -> ``FemgpuError`` carrying
+  ``.code`` and the native message, ``Form`` owning a ``femgpu_form*``;
+* the emitted element kernel `void kernel(double* outputs..., const double*
+  tables..., double constants...)` called through the harness's uniform
+  `kernel_argv(o, t, c)` (proj/tests/test_backend.cpp:62-98) ->
+  ``Form.kernel_argv`` with the same argument order (emit_c.cpp:137-140) and
+  the same `+=` semantics.
+
+The CUDA path is the only path: if ``libfemgpu.so`` is missing this module
+raises at load time; there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import fe
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libfemgpu.so")
+
+SCHED_AUTO, SCHED_TENSOR, SCHED_QUADRATURE = 0, 1, 2
+SCHEDULE_NAMES = {SCHED_AUTO: "auto", SCHED_TENSOR: "tensor", SCHED_QUADRATURE: "quadrature"}
+
+ERROR_NAMES = {
+    0: "OK", 1: "PARSE", 2: "UNKNOWN_LOOP", 3: "NOT_FEM_NEST", 4: "NON_DISTRIBUTABLE",
+    5: "NON_SEPARABLE", 6: "NOT_NORMAL_FORM", 7: "TOO_MANY_MONOMIALS", 8: "INCONSISTENT_LAYOUT",
+    9: "INVALID_ARG", 10: "IO", 11: "INTERNAL", 12: "CUDA", 13: "NO_DEVICE", 14: "UNSUPPORTED",
+}
+
+# Every symbol include/femgpu.h declares (checked by tests/test_abi.py).
+EXPORTS = ("femgpu_form_create", "femgpu_form_free", "femgpu_form_get_info", "femgpu_assemble",
+           "femgpu_assemble_host", "femgpu_kernel_argv", "femgpu_kernel_argc",
+           "femgpu_kernel_argname", "femgpu_last_error", "femgpu_version")
+
+
+class FemgpuError(RuntimeError):
+    """A non-zero femgpu return code (femopt.h:20-33 meanings for 1..11)."""
+
+    def __init__(self, code: int, message: str):
+        super().__init__(f"femgpu error {code} ({ERROR_NAMES.get(code, '?')}): {message}")
+        self.code = code
+        self.message = message
+
+
+class FormDesc(C.Structure):
+    _fields_ = [("kind", C.c_int), ("nq", C.c_int), ("ns", C.c_int), ("nc", C.c_int),
+                ("W", C.POINTER(C.c_double)), ("B", C.POINTER(C.c_double)),
+                ("D", C.POINTER(C.c_double)), ("P", C.POINTER(C.c_double)),
+                ("consts", C.c_double * 4), ("schedule", C.c_int)]
+
+
+class FormInfo(C.Structure):
+    _fields_ = [("n", C.c_int), ("ncoef", C.c_int), ("schedule", C.c_int),
+                ("flops_per_cell", C.c_double), ("bytes_per_cell", C.c_double),
+                ("kernels_per_launch", C.c_int), ("kernel_name", C.c_char * 64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libfemgpu.so (built by __graft_entry__.build()); fail loudly if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise FileNotFoundError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ "
+                                    "as g; g.build()'` (no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        vp, dp = C.c_void_p, C.POINTER(C.c_double)
+        L.femgpu_form_create.argtypes = [C.POINTER(FormDesc), C.POINTER(vp)]
+        L.femgpu_form_free.argtypes = [vp]
+        L.femgpu_form_free.restype = None
+        L.femgpu_form_get_info.argtypes = [vp, C.POINTER(FormInfo)]
+        L.femgpu_assemble.argtypes = [vp, C.c_long, vp, vp, vp, C.c_int, vp]
+        L.femgpu_assemble_host.argtypes = [vp, C.c_long, dp, dp, dp, C.c_int]
+        L.femgpu_kernel_argv.argtypes = [vp, C.c_long, C.POINTER(dp), C.POINTER(dp), dp]
+        L.femgpu_kernel_argc.argtypes = [vp, C.c_int, C.POINTER(C.c_int)]
+        L.femgpu_kernel_argname.argtypes = [vp, C.c_int, C.c_int, C.c_char_p, C.c_size_t]
+        L.femgpu_last_error.restype = C.c_char_p
+        L.femgpu_version.restype = C.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise FemgpuError(rc, lib().femgpu_last_error().decode())
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _devptr(x):
+    """Device pointer of a torch CUDA tensor (or an int)."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    return x.data_ptr()
+
+
+class Form:
+    """A femgpu form (element-kernel family) bound to the current CUDA device."""
+
+    def __init__(self, kind: int, tables: "fe.Tables", consts=(), schedule: int = SCHED_AUTO):
+        self.kind = kind
+        self._keep = [np.ascontiguousarray(tables.W, dtype=np.float64),
+                      np.ascontiguousarray(tables.B, dtype=np.float64),
+                      np.ascontiguousarray(tables.D, dtype=np.float64),
+                      np.ascontiguousarray(tables.P, dtype=np.float64)]
+        W, B, D, P = self._keep
+        d = FormDesc()
+        d.kind, d.nq, d.ns, d.nc = kind, W.shape[0], B.shape[1], P.shape[1]
+        d.W, d.B, d.D, d.P = _dptr(W), _dptr(B), _dptr(D), _dptr(P)
+        cs = list(consts) + [0.0] * (4 - len(consts))
+        d.consts = (C.c_double * 4)(*cs)
+        d.schedule = schedule
+        self.h = C.c_void_p()
+        _check(lib().femgpu_form_create(C.byref(d), C.byref(self.h)))
+        inf = FormInfo()
+        _check(lib().femgpu_form_get_info(self.h, C.byref(inf)))
+        self.n, self.ncoef = inf.n, inf.ncoef
+        self.info = {"n": inf.n, "ncoef": inf.ncoef, "schedule": SCHEDULE_NAMES[inf.schedule],
+                     "flops_per_cell": inf.flops_per_cell, "bytes_per_cell": inf.bytes_per_cell,
+                     "kernels_per_launch": inf.kernels_per_launch,
+                     "kernel_name": inf.kernel_name.decode()}
+
+    @classmethod
+    def from_config(cls, cfg: "fe.Config", tables: "fe.Tables | None" = None,
+                    schedule: int = SCHED_AUTO) -> "Form":
+        return cls(cfg.kind, tables or fe.tables(cfg), cfg.consts, schedule)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().femgpu_form_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- device path (the hot path) ------------------------------------------
+    def assemble(self, coords, coeffs, out, ncells: int | None = None, accumulate: bool = False,
+                 stream=None):
+        """Element matrices into ``out`` (device tensors; cell-major layouts)."""
+        E = int(coords.shape[0]) if ncells is None else int(ncells)
+        s = None if stream is None else (stream if isinstance(stream, int) else stream.cuda_stream)
+        _check(lib().femgpu_assemble(self.h, E, _devptr(coords), _devptr(coeffs), _devptr(out),
+                                     int(accumulate), s))
+
+    # -- host path (end to end) ----------------------------------------------
+    def assemble_host(self, coords: np.ndarray, coeffs: np.ndarray, out: np.ndarray | None = None,
+                      accumulate: bool = False) -> np.ndarray:
+        coords = np.ascontiguousarray(coords, dtype=np.float64)
+        coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+        E = coords.shape[0]
+        if out is None:
+            out = np.zeros((E, self.n, self.n))
+        _check(lib().femgpu_assemble_host(self.h, E, _dptr(coords), _dptr(coeffs), _dptr(out),
+                                          int(accumulate)))
+        return out
+
+    def assemble_host_ptr(self, E: int, coords_ptr: int, coeffs_ptr: int, out_ptr: int,
+                          accumulate: bool = False):
+        """Same with raw host pointers (pinned torch tensors in bench.py)."""
+        dp = C.POINTER(C.c_double)
+        _check(lib().femgpu_assemble_host(self.h, E, C.cast(coords_ptr, dp), C.cast(coeffs_ptr, dp),
+                                          C.cast(out_ptr, dp), int(accumulate)))
+
+    # -- emitted-C interface (femopt's element kernel signature) ---------------
+    def argnames(self):
+        out = []
+        for group in range(3):
+            cnt = C.c_int()
+            _check(lib().femgpu_kernel_argc(self.h, group, C.byref(cnt)))
+            names = []
+            buf = C.create_string_buffer(64)
+            for i in range(cnt.value):
+                _check(lib().femgpu_kernel_argname(self.h, group, i, buf, 64))
+                names.append(buf.value.decode())
+            out.append(names)
+        return tuple(out)
+
+    def kernel_argv(self, ncells: int, outputs, tables, constants=()):
+        """Call like the emitted C: outputs += kernel(tables, constants)."""
+        outs = [np.ascontiguousarray(o) for o in outputs]
+        for o, oo in zip(outs, outputs):
+            if o is not oo:
+                raise ValueError("outputs must be C-contiguous float64 arrays (updated in place)")
+        tabs = [np.ascontiguousarray(t, dtype=np.float64) for t in tables]
+        cons = np.ascontiguousarray(list(constants) or [0.0], dtype=np.float64)
+        dp = C.POINTER(C.c_double)
+        op = (dp * len(outs))(*[_dptr(o) for o in outs])
+        tp = (dp * len(tabs))(*[_dptr(t) for t in tabs])
+        _check(lib().femgpu_kernel_argv(self.h, ncells, op, tp, _dptr(cons)))
+
+
+def version() -> str:
+    return lib().femgpu_version().decode()

@@ -1,0 +1,144 @@
+// fp64_peak.cu -- measures the B200's FP64 DFMA and DMMA (mma.sync .f64) peaks.
+//
+// MEASURED_PEAKS.json carries only HBM and bf16; the FP64
+// roofline denominators of the element kernels come from this tool.  Each
+// variant runs many independent accumulation chains per warp on every SM and
+// reports FLOP/s (DFMA = 2 flops per lane; mma mMnNkK = 2*M*N*K per warp).
+// Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o fp64_peak fp64_peak.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { \
+  printf("CUDA error %s at %d\n", cudaGetErrorString(e), __LINE__); return 1; } } while (0)
+
+template <int CHAINS>
+__global__ void dfma_kernel(double* out, int iters, double a, double b) {
+  double acc[CHAINS];
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) acc[c] = threadIdx.x * 1e-3 + c;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int c = 0; c < CHAINS; ++c) acc[c] = fma(acc[c], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) s += acc[c];
+  if (s == 12345.678) out[0] = s;
+}
+
+template <int CHAINS>
+__global__ void dmma_m8n8k4(double* out, int iters) {
+  double a = threadIdx.x * 1e-3, b = 1.0 - threadIdx.x * 1e-4;
+  double c0[CHAINS], c1[CHAINS];
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) { c0[c] = c; c1[c] = -c; }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int c = 0; c < CHAINS; ++c)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(c0[c]), "+d"(c1[c]) : "d"(a), "d"(b));
+  }
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) s += c0[c] + c1[c];
+  if (s == 12345.678) out[0] = s;
+}
+
+template <int CHAINS>
+__global__ void dmma_m16n8k8(double* out, int iters) {
+  double a[4], b[2];
+  for (int i = 0; i < 4; ++i) a[i] = threadIdx.x * 1e-3 + i;
+  for (int i = 0; i < 2; ++i) b[i] = 1.0 - threadIdx.x * 1e-4 * i;
+  double c[CHAINS][4];
+#pragma unroll
+  for (int k = 0; k < CHAINS; ++k) for (int i = 0; i < 4; ++i) c[k][i] = k + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < CHAINS; ++k)
+      asm volatile("mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+                   : "+d"(c[k][0]), "+d"(c[k][1]), "+d"(c[k][2]), "+d"(c[k][3])
+                   : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < CHAINS; ++k) for (int i = 0; i < 4; ++i) s += c[k][i];
+  if (s == 12345.678) out[0] = s;
+}
+
+template <int CHAINS>
+__global__ void dmma_m16n8k16(double* out, int iters) {
+  double a[8], b[4];
+  for (int i = 0; i < 8; ++i) a[i] = threadIdx.x * 1e-3 + i;
+  for (int i = 0; i < 4; ++i) b[i] = 1.0 - threadIdx.x * 1e-4 * i;
+  double c[CHAINS][4];
+#pragma unroll
+  for (int k = 0; k < CHAINS; ++k) for (int i = 0; i < 4; ++i) c[k][i] = k + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < CHAINS; ++k)
+      asm volatile("mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7,%8,%9,%10,%11}, {%12,%13,%14,%15}, {%0,%1,%2,%3};\n"
+                   : "+d"(c[k][0]), "+d"(c[k][1]), "+d"(c[k][2]), "+d"(c[k][3])
+                   : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]),
+                     "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < CHAINS; ++k) for (int i = 0; i < 4; ++i) s += c[k][i];
+  if (s == 12345.678) out[0] = s;
+}
+
+__global__ void copy_kernel(const double2* __restrict__ a, double2* __restrict__ b, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    b[i] = a[i];
+}
+
+template <typename F>
+static float time_it(F launch, int reps) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  launch();  // warm-up
+  cudaDeviceSynchronize();
+  float best = 1e30f;
+  for (int r = 0; r < reps; ++r) {
+    cudaEventRecord(e0);
+    launch();
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best) best = ms;
+  }
+  return best;
+}
+
+int main() {
+  cudaDeviceProp p; CK(cudaGetDeviceProperties(&p, 0));
+  int sms = p.multiProcessorCount;
+  printf("device %s, %d SMs\n", p.name, sms);
+  double* out; CK(cudaMalloc(&out, 8));
+  const int iters = 4096;
+  for (int tpb : {256, 512}) for (int bps : {1, 2, 4}) {
+    int grid = sms * bps;
+    float ms = time_it([&] { dfma_kernel<8><<<grid, tpb>>>(out, iters, 0.999, 1e-3); }, 5);
+    double fl = 2.0 * 8 * iters * (double)grid * tpb;
+    printf("DFMA  tpb=%d blocks/SM=%d: %.2f TFLOP/s\n", tpb, bps, fl / ms / 1e9);
+  }
+  for (int tpb : {128, 256, 512}) for (int bps : {1, 2, 4}) {
+    int grid = sms * bps;
+    float ms = time_it([&] { dmma_m8n8k4<8><<<grid, tpb>>>(out, iters); }, 5);
+    double fl = 2.0 * 8 * 8 * 4 * 8 * iters * (double)grid * (tpb / 32);
+    printf("DMMA m8n8k4   tpb=%d blocks/SM=%d: %.2f TFLOP/s\n", tpb, bps, fl / ms / 1e9);
+    ms = time_it([&] { dmma_m16n8k8<4><<<grid, tpb>>>(out, iters); }, 5);
+    fl = 2.0 * 16 * 8 * 8 * 4 * iters * (double)grid * (tpb / 32);
+    printf("DMMA m16n8k8  tpb=%d blocks/SM=%d: %.2f TFLOP/s\n", tpb, bps, fl / ms / 1e9);
+    ms = time_it([&] { dmma_m16n8k16<4><<<grid, tpb>>>(out, iters / 2); }, 5);
+    fl = 2.0 * 16 * 8 * 16 * 4 * (iters / 2) * (double)grid * (tpb / 32);
+    printf("DMMA m16n8k16 tpb=%d blocks/SM=%d: %.2f TFLOP/s\n", tpb, bps, fl / ms / 1e9);
+  }
+  size_t n = (size_t)1 << 27;  // 2 GiB per buffer (double2)
+  double2 *a, *b;
+  CK(cudaMalloc(&a, n * 16)); CK(cudaMalloc(&b, n * 16));
+  cudaMemset(a, 0, n * 16);
+  float ms = time_it([&] { copy_kernel<<<sms * 8, 512>>>(a, b, n); }, 5);
+  printf("copy (read+write) %.1f GB/s\n", 2.0 * n * 16 / ms / 1e6);
+  return 0;
+}

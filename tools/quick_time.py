@@ -1,0 +1,51 @@
+#!/usr/bin/env python3
+"""Quick device timing of each config's kernel (development aid, not the bench)."""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_1604_05872_b200 import fe, femgpu  # noqa: E402
+
+
+def main(names):
+    dev = torch.device("cuda:0")
+    for name in names:
+        cfg = fe.CONFIGS[name]
+        t0 = time.time()
+        coords, coeffs = fe.cell_inputs(cfg)
+        try:
+            form = femgpu.Form.from_config(cfg)
+        except femgpu.FemgpuError as e:
+            print(json.dumps({"config": name, "error": str(e)}))
+            continue
+        x = torch.from_numpy(coords).to(dev)
+        c = torch.from_numpy(coeffs).to(dev)
+        E = coords.shape[0]
+        out = torch.empty((E, cfg.n, cfg.n), dtype=torch.float64, device=dev)
+        for _ in range(3):
+            form.assemble(x, c, out)
+        torch.cuda.synchronize()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        times = []
+        for _ in range(10):
+            ev[0].record()
+            form.assemble(x, c, out)
+            ev[1].record()
+            torch.cuda.synchronize()
+            times.append(ev[0].elapsed_time(ev[1]) / 1e3)
+        t = sorted(times)[len(times) // 2]
+        bpc = cfg.bytes_per_cell()
+        fpc = form.info["flops_per_cell"]
+        print(json.dumps({"config": name, "cells": E, "ms": round(t * 1e3, 4),
+                          "Mcells_s": round(E / t / 1e6, 2), "GB_s": round(E * bpc / t / 1e9, 1),
+                          "GFLOP_s": round(E * fpc / t / 1e9, 1), "flops_per_cell": fpc,
+                          "kernel": form.info["kernel_name"], "setup_s": round(time.time() - t0, 1)}),
+              flush=True)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:] or list(fe.CONFIGS))
