@@ -330,7 +330,7 @@ int femgpu_form_create(const femgpu_form_desc* d, femgpu_form** out) {
     std::vector<double> host;
     switch (d->kind) {
       case FEMGPU_HELMHOLTZ:
-        if (d->ns == 4 && d->nc <= 4 && constant_gradients(f.get()) &&
+        if (d->ns == 4 && d->nc == 4 && constant_gradients(f.get()) &&
             d->schedule != FEMGPU_SCHED_QUADRATURE) {
           f->route = ROUTE_HELM_P1;
           build_helm_p1(f.get());
@@ -364,7 +364,11 @@ int femgpu_form_create(const femgpu_form_desc* d, femgpu_form** out) {
           throw Error(FEMGPU_ERR_UNSUPPORTED, "no Burgers kernel for this size/schedule");
         f->route = ROUTE_BURGERS;
         f->schedule = FEMGPU_SCHED_TENSOR;
-        throw Error(FEMGPU_ERR_UNSUPPORTED, "Burgers kernel not built yet");
+        host.assign(femgpu::burgers_table_doubles(), 0.0);
+        femgpu::burgers_tables(f->nq, f->W.data(), f->B.data(), f->D.data(), host.data());
+        // GEMM-1: 3 c x 20 n x 630 (a,p); GEMM-2: 67 x 400; epilogue 3 x 210 x 3 x 4
+        f->flops_per_cell = 2.0 * 3 * 20 * 630 + 2.0 * 67 * 400 + 3.0 * 210 * 3 * 4 + 60 * 7 + 60;
+        f->kernel_name = "burgers_kernel";
     }
     if (!host.empty()) {
       f->tab_doubles = host.size();

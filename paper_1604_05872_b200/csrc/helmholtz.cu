@@ -30,83 +30,122 @@
 namespace femgpu {
 
 // ============================================================================
-// P1: thread per cell
+// P1: thread per cell, persistent CTAs, TMA bulk-copy input ring
 // ============================================================================
-constexpr int P1_TILE = 128;
-constexpr int P1_SX = 14;  // padded smem strides (doubles): conflict-free 16B accesses
-constexpr int P1_SF = 6;
-constexpr int P1_SO = 18;
+constexpr int P1_TILE = 128;      // cells per tile = threads per CTA
+constexpr int P1_NBUF = 3;        // input stages in flight per CTA
+constexpr int P1_CTAS = 3;        // CTAs per SM
+constexpr int P1_SO = 18;         // padded output staging stride: conflict-free 16B stores
+constexpr int P1_IN = P1_TILE * 16;                       // doubles per input stage
+constexpr size_t P1_SMEM = sizeof(double) * (P1_NBUF * P1_IN + P1_TILE * P1_SO) +
+                           P1_NBUF * sizeof(uint64_t);
 
-__global__ void __launch_bounds__(P1_TILE) helm_p1_kernel(HelmP1Params prm, long E,
-                                                          const double* __restrict__ coords,
-                                                          const double* __restrict__ coef,
-                                                          double* __restrict__ A, int acc) {
-  __shared__ __align__(16) double sx[P1_TILE * P1_SX];
-  __shared__ __align__(16) double sf[P1_TILE * P1_SF];
-  __shared__ __align__(16) double so[P1_TILE * P1_SO];
-  const long e0 = (long)blockIdx.x * P1_TILE;
-  const int nt = (int)min((long)P1_TILE, E - e0);
+__global__ void __launch_bounds__(P1_TILE, P1_CTAS)
+    helm_p1_kernel(HelmP1Params prm, long E, const double* __restrict__ coords,
+                   const double* __restrict__ coef, double* __restrict__ A, int acc) {
+  extern __shared__ __align__(16) double smem[];
+  double* sIn = smem;                               // [NBUF][coords 128x12 | f 128x4]
+  double* so = smem + P1_NBUF * P1_IN;              // [128][18]
+  uint64_t* full = reinterpret_cast<uint64_t*>(so + P1_TILE * P1_SO);
   const int tid = threadIdx.x;
-  {
-    const double2* gx = reinterpret_cast<const double2*>(coords + e0 * 12);
-    for (int i = tid; i < nt * 6; i += P1_TILE) {
-      double2 v = ldg_stream(gx + i);
-      *reinterpret_cast<double2*>(&sx[(i / 6) * P1_SX + 2 * (i % 6)]) = v;
-    }
-    const double2* gf = reinterpret_cast<const double2*>(coef + e0 * 4);
-    for (int i = tid; i < nt * 2; i += P1_TILE) {
-      double2 v = ldg_stream(gf + i);
-      *reinterpret_cast<double2*>(&sf[(i / 2) * P1_SF + 2 * (i % 2)]) = v;
-    }
+  const long ntiles = (E + P1_TILE - 1) / P1_TILE;
+  if ((long)blockIdx.x >= ntiles) return;
+  if (tid == 0) {
+    for (int b = 0; b < P1_NBUF; ++b) mbar_init(&full[b], 1);
+    fence_mbar_init();
   }
   __syncthreads();
-  if (tid < nt) {
-    const Geo geo = cell_geometry(&sx[tid * P1_SX]);
-    const double f[4] = {sf[tid * P1_SF + 0], sf[tid * P1_SF + 1], sf[tid * P1_SF + 2],
-                         sf[tid * P1_SF + 3]};
-    double g[4][3];
+  auto issue = [&](long tile, int b) {  // both inputs of a tile: contiguous, 16B multiples
+    const long e0 = tile * P1_TILE;
+    const int nt = (int)min((long)P1_TILE, E - e0);
+    double* dst = sIn + b * P1_IN;
+    mbar_expect_tx(&full[b], nt * 128);
+    bulk_g2s(dst, coords + e0 * 12, nt * 96, &full[b]);
+    bulk_g2s(dst + P1_TILE * 12, coef + e0 * 4, nt * 32, &full[b]);
+  };
+  if (tid == 0)
+    for (int b = 0; b < P1_NBUF; ++b) {
+      const long tl = blockIdx.x + (long)b * gridDim.x;
+      if (tl < ntiles) issue(tl, b);
+    }
+  long it = 0;
+  for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int b = (int)(it % P1_NBUF);
+    const long e0 = tile * P1_TILE;
+    const int nt = (int)min((long)P1_TILE, E - e0);
+    mbar_wait(&full[b], (uint32_t)((it / P1_NBUF) & 1));
+    const double* sx = sIn + b * P1_IN;
+    const double* sf = sx + P1_TILE * 12;
+    if (tid < nt) {
+      double x[12];
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int b = 0; b < 3; ++b)
-        g[j][b] = geo.K[0][b] * prm.Dr[j][0] + geo.K[1][b] * prm.Dr[j][1] +
-                  geo.K[2][b] * prm.Dr[j][2];
-    const double fbar = f[0] * prm.c[0] + f[1] * prm.c[1] + f[2] * prm.c[2] + f[3] * prm.c[3];
-    double out[16];
-    int p = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int k = j; k < 4; ++k, ++p) {
-        double st = g[j][0] * g[k][0] + g[j][1] * g[k][1] + g[j][2] * g[k][2];
-        double ms = f[0] * prm.M[0][p] + f[1] * prm.M[1][p] + f[2] * prm.M[2][p] +
-                    f[3] * prm.M[3][p];
-        double v = geo.adet * (fbar * st + ms);
-        out[j * 4 + k] = v;
-        out[k * 4 + j] = v;
+      for (int i = 0; i < 6; ++i) {
+        const double2 v = reinterpret_cast<const double2*>(sx + tid * 12)[i];
+        x[2 * i] = v.x;
+        x[2 * i + 1] = v.y;
       }
+      const double2 f01 = reinterpret_cast<const double2*>(sf + tid * 4)[0];
+      const double2 f23 = reinterpret_cast<const double2*>(sf + tid * 4)[1];
+      const double f[4] = {f01.x, f01.y, f23.x, f23.y};
+      const Geo geo = cell_geometry(x);
+      double g[4][3];
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
-      *reinterpret_cast<double2*>(&so[tid * P1_SO + 2 * i]) = make_double2(out[2 * i], out[2 * i + 1]);
-  }
-  __syncthreads();
-  double2* gA = reinterpret_cast<double2*>(A + e0 * 16);
-  for (int i = tid; i < nt * 8; i += P1_TILE) {
-    double2 v = *reinterpret_cast<const double2*>(&so[(i / 8) * P1_SO + 2 * (i % 8)]);
-    if (acc) {
-      double2 o = gA[i];
-      v.x += o.x;
-      v.y += o.y;
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int bb = 0; bb < 3; ++bb)
+          g[j][bb] = geo.K[0][bb] * prm.Dr[j][0] + geo.K[1][bb] * prm.Dr[j][1] +
+                     geo.K[2][bb] * prm.Dr[j][2];
+      const double fbar = f[0] * prm.c[0] + f[1] * prm.c[1] + f[2] * prm.c[2] + f[3] * prm.c[3];
+      double out[16];
+      int p = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int k = j; k < 4; ++k, ++p) {
+          const double st = g[j][0] * g[k][0] + g[j][1] * g[k][1] + g[j][2] * g[k][2];
+          const double ms = f[0] * prm.M[0][p] + f[1] * prm.M[1][p] + f[2] * prm.M[2][p] +
+                            f[3] * prm.M[3][p];
+          const double v = geo.adet * (fbar * st + ms);
+          out[j * 4 + k] = v;
+          out[k * 4 + j] = v;
+        }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        *reinterpret_cast<double2*>(&so[tid * P1_SO + 2 * i]) = make_double2(out[2 * i], out[2 * i + 1]);
     }
-    stg_stream(gA + i, v);
+    __syncthreads();  // staging complete; input stage b fully consumed
+    if (tid == 0) {
+      const long nx = tile + (long)P1_NBUF * gridDim.x;
+      if (nx < ntiles) issue(nx, b);
+    }
+    double2* gA = reinterpret_cast<double2*>(A + e0 * 16);
+    for (int i = tid; i < nt * 8; i += P1_TILE) {
+      double2 v = *reinterpret_cast<const double2*>(&so[(i / 8) * P1_SO + 2 * (i % 8)]);
+      if (acc) {
+        const double2 o = gA[i];
+        v.x += o.x;
+        v.y += o.y;
+      }
+      stg_stream(gA + i, v);
+    }
+    __syncthreads();  // staging free for the next tile
   }
 }
 
 cudaError_t launch_helm_p1(const HelmP1Params& prm, long E, const double* coords,
                            const double* coef, double* A, int acc, cudaStream_t s) {
   if (E <= 0) return cudaSuccess;
-  long grid = (E + P1_TILE - 1) / P1_TILE;
-  helm_p1_kernel<<<(unsigned)grid, P1_TILE, 0, s>>>(prm, E, coords, coef, A, acc);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(helm_p1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)P1_SMEM);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const long ntiles = (E + P1_TILE - 1) / P1_TILE;
+  const long maxc = (long)P1_CTAS * kNumSMs;
+  const int grid = (int)(ntiles < maxc ? ntiles : maxc);
+  helm_p1_kernel<<<grid, P1_TILE, P1_SMEM, s>>>(prm, E, coords, coef, A, acc);
   return cudaGetLastError();
 }
 
@@ -116,23 +155,25 @@ cudaError_t launch_helm_p1(const HelmP1Params& prm, long E, const double* coords
 template <int NS, int NC>
 struct HelmTensorShape {
   static constexpr int NP = NS * (NS + 1) / 2;          // symmetric half of A_e
-  static constexpr int NT = ((NP + 15) / 16) * 2;       // n8 tiles, even (2 n-halves)
-  static constexpr int NTW = NT / 2;                    // n8 tiles per warp
+  static constexpr int NT = ((NP + 7) / 8 + 1) / 2 * 2;  // n8 tiles (even)
   static constexpr int KR = 7 * NC;                     // alpha = (m, s)
   static constexpr int KPS = 2;                         // k8 steps per pipeline stage
   static constexpr int KS = ((KR + 8 * KPS - 1) / (8 * KPS)) * KPS;  // k8 steps (padded)
   static constexpr int NSTG = KS / KPS;                 // stages per tile
-  static constexpr int NBUF = 3;                        // pipeline depth
-  static constexpr int MT = 4;                          // m16 tiles per CTA
+  static constexpr int NBUF = 2;                        // pipeline depth
+  static constexpr int MT = 2;                          // m16 tiles per CTA
   static constexpr int CELLS = 16 * MT;                 // cells per CTA tile
-  static constexpr int THREADS = 256;                   // 8 warps = MT x 2 n-halves
+  static constexpr int THREADS = 256;                   // 8 warps, n-tiles interleaved
+  static constexpr int WARPS = THREADS / 32;
+  static constexpr int NTW = (NT + WARPS - 1) / WARPS;  // max n8 tiles per warp
   static constexpr int STAGE_DBL = KPS * NT * 64;       // doubles per B stage
   static constexpr int A_DBL = MT * KS * 128;           // fragment-native g tile
   static constexpr int IN_DBL = CELLS * (12 + NC);      // raw inputs of a tile
-  static constexpr int STAGE_OUT_DBL = 16 * NS * NS;    // epilogue staging (aliases A)
-  static_assert(STAGE_OUT_DBL <= A_DBL, "epilogue staging must fit in the A region");
+  static constexpr int RS = NS * NS + 6;                // staging row stride (fewer conflicts)
+  static constexpr int OUTC = 8;                        // cells per epilogue round
+  static_assert(OUTC * RS <= A_DBL, "epilogue staging must fit in the A region");
   static constexpr size_t SMEM = sizeof(double) * (size_t)(A_DBL + NBUF * STAGE_DBL + IN_DBL) +
-                                 NBUF * sizeof(uint64_t) + NP * sizeof(int);
+                                 2 * NBUF * sizeof(uint64_t) + NP * sizeof(int);
 };
 
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
@@ -141,9 +182,12 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
 
 template <int NS, int NC>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(256, 2)
     helm_tensor_kernel(long E, const double* __restrict__ coords, const double* __restrict__ coef,
                        const double* __restrict__ Sfrag, double* __restrict__ A, int acc) {
   using Sh = HelmTensorShape<NS, NC>;
@@ -151,40 +195,45 @@ __global__ void __launch_bounds__(256, 1)
   double* sA = smem;                                  // [MT][KS][32][4]
   double* sB = sA + Sh::A_DBL;                        // [NBUF][KPS][NT][32][2]
   double* sIn = sB + Sh::NBUF * Sh::STAGE_DBL;        // [CELLS][12] then [CELLS][NC]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sIn + Sh::IN_DBL);
-  int* sPair = reinterpret_cast<int*>(bar + Sh::NBUF);  // p -> (j*NS+k) | (k*NS+j) << 16
+  uint64_t* full = reinterpret_cast<uint64_t*>(sIn + Sh::IN_DBL);
+  uint64_t* empty = full + Sh::NBUF;
+  int* sPair = reinterpret_cast<int*>(empty + Sh::NBUF);  // p -> (j*NS+k) | (k*NS+j) << 16
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int mt = warp & 3, nh = warp >> 2;
   const int g = lane >> 2, t = lane & 3;
   const long ntiles = (E + Sh::CELLS - 1) / Sh::CELLS;
   if ((long)blockIdx.x >= ntiles) return;
 
   if (tid == 0) {
-    for (int b = 0; b < Sh::NBUF; ++b) mbar_init(&bar[b], 1);
+    for (int b = 0; b < Sh::NBUF; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], Sh::WARPS);
+    }
     fence_mbar_init();
   }
   for (int j = 0, p = 0; j < NS; ++j)
     for (int k = j; k < NS; ++k, ++p)
       if (p % Sh::THREADS == tid) sPair[p] = (j * NS + k) | ((k * NS + j) << 16);
   __syncthreads();
-  // Stage loads this CTA will consume; never leave a bulk copy in flight at exit.
+
+  // B pipeline: loads numbered globally, load i carries k-chunk i % NSTG into
+  // buffer i % NBUF.  full[b]: TMA transaction count; empty[b]: one arrival per
+  // warp once it has consumed the buffer.  Never leave a copy in flight at exit.
   const long my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
   const long total_loads = my_tiles * Sh::NSTG;
-  // B pipeline: stage loads are numbered globally; load i carries k-chunk i % NSTG.
   long issued = 0;
   auto issue = [&](long i) {
     const int b = (int)(i % Sh::NBUF);
+    if (i >= Sh::NBUF) mbar_wait(&empty[b], (uint32_t)(((i / Sh::NBUF) - 1) & 1));
     const int chunk = (int)(i % Sh::NSTG);
-    mbar_expect_tx(&bar[b], Sh::STAGE_DBL * 8);
+    mbar_expect_tx(&full[b], Sh::STAGE_DBL * 8);
     bulk_g2s(sB + b * Sh::STAGE_DBL, Sfrag + (size_t)chunk * Sh::STAGE_DBL, Sh::STAGE_DBL * 8,
-             &bar[b]);
+             &full[b]);
   };
   if (tid == 0)
     for (; issued < Sh::NBUF && issued < total_loads; ++issued) issue(issued);
   long consumed = 0;
 
-  // raw inputs of a tile -> sIn (cp.async, 8-byte granularity: any alignment/tail)
   auto load_inputs = [&](long tile) {
     const long c0 = tile * Sh::CELLS;
     const int nt = (int)min((long)Sh::CELLS, E - c0);
@@ -195,123 +244,145 @@ __global__ void __launch_bounds__(256, 1)
   };
   load_inputs(blockIdx.x);
 
+  // n-tiles of this warp: warp, warp+8, ... (balanced across the 4 SM sub-partitions)
+  int ntw = 0;
+  for (int nt_ = warp; nt_ < Sh::NT; nt_ += Sh::WARPS) ++ntw;
+
   for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const long c0 = tile * Sh::CELLS;
     const int nt = (int)min((long)Sh::CELLS, E - c0);
     cp_async_wait_all();
     __syncthreads();
-    // ---- prologue: g[cell][alpha] -> sA (fragment-native), 4 threads per cell
+    // ---- prologue: g[cell][alpha] -> sA (fragment-native), 8 threads per cell
     {
-      const int cell = tid >> 2, part = tid & 3;
+      const int cell = tid >> 3, part = tid & 7;
+      constexpr int MPT = (NC + 7) / 8;
       double Gs[7];
-      double fv[(NC + 3) / 4];
+      double fv[MPT];
       if (cell < nt) {
         const Geo geo = cell_geometry(&sIn[cell * 12]);
         const double(*K)[3] = geo.K;
-        const int ab[6][2] = {{0, 0}, {1, 1}, {2, 2}, {0, 1}, {0, 2}, {1, 2}};
 #pragma unroll
         for (int s = 0; s < 6; ++s) {
-          const int a = ab[s][0], b = ab[s][1];
+          const int a = s < 3 ? s : (s == 5 ? 1 : 0);
+          const int b = s < 3 ? s : (s == 3 ? 1 : 2);
           Gs[s] = geo.adet * (K[a][0] * K[b][0] + K[a][1] * K[b][1] + K[a][2] * K[b][2]);
         }
         Gs[6] = geo.adet;
 #pragma unroll
-        for (int i = 0; i < (NC + 3) / 4; ++i) {
-          const int m = part + 4 * i;
+        for (int i = 0; i < MPT; ++i) {
+          const int m = part + 8 * i;
           fv[i] = m < NC ? sIn[Sh::CELLS * 12 + cell * NC + m] : 0.0;
         }
       } else {
 #pragma unroll
         for (int s = 0; s < 7; ++s) Gs[s] = 0.0;
 #pragma unroll
-        for (int i = 0; i < (NC + 3) / 4; ++i) fv[i] = 0.0;
+        for (int i = 0; i < MPT; ++i) fv[i] = 0.0;
       }
       const int cmt = cell >> 4, rr = cell & 15;
       const int gg = rr & 7, vrow = rr >> 3;
 #pragma unroll
-      for (int i = 0; i < (NC + 3) / 4; ++i) {
-        const int m = part + 4 * i;
-        if (m >= NC) break;
+      for (int i = 0; i < MPT; ++i) {
+        const int m = part + 8 * i;
+        if (m < NC) {
 #pragma unroll
-        for (int s = 0; s < 7; ++s) {
-          const int alpha = m * 7 + s;
-          const int ks = alpha >> 3, kk = alpha & 7;
-          const int ln = gg * 4 + (kk & 3), v = vrow + 2 * (kk >> 2);
-          sA[((cmt * Sh::KS + ks) * 32 + ln) * 4 + v] = fv[i] * Gs[s];
+          for (int s = 0; s < 7; ++s) {
+            const int alpha = m * 7 + s;
+            const int ks = alpha >> 3, kk = alpha & 7;
+            const int ln = gg * 4 + (kk & 3), v = vrow + 2 * (kk >> 2);
+            sA[((cmt * Sh::KS + ks) * 32 + ln) * 4 + v] = fv[i] * Gs[s];
+          }
         }
       }
-      // zero the K padding [KR, 8*KS)
-      for (int alpha = Sh::KR + part; alpha < 8 * Sh::KS; alpha += 4) {
+      for (int alpha = Sh::KR + part; alpha < 8 * Sh::KS; alpha += 8) {  // zero K padding
         const int ks = alpha >> 3, kk = alpha & 7;
         const int ln = gg * 4 + (kk & 3), v = vrow + 2 * (kk >> 2);
         sA[((cmt * Sh::KS + ks) * 32 + ln) * 4 + v] = 0.0;
       }
     }
     __syncthreads();
-    // prefetch the next tile's raw inputs while the tensor cores run
     if (tile + gridDim.x < ntiles) load_inputs(tile + gridDim.x);
 
-    // ---- main loop: C[16 x 8*NTW] per warp on the FP64 tensor cores
-    double c[Sh::NTW][4];
+    // ---- main loop: every warp computes all MT m-tiles x its n-tiles ---------
+    double c[Sh::MT][Sh::NTW][4];
 #pragma unroll
-    for (int i = 0; i < Sh::NTW; ++i) c[i][0] = c[i][1] = c[i][2] = c[i][3] = 0.0;
+    for (int mt = 0; mt < Sh::MT; ++mt)
+#pragma unroll
+      for (int i = 0; i < Sh::NTW; ++i) c[mt][i][0] = c[mt][i][1] = c[mt][i][2] = c[mt][i][3] = 0.0;
+#pragma unroll 1
     for (int st = 0; st < Sh::NSTG; ++st) {
       const int b = (int)(consumed % Sh::NBUF);
-      mbar_wait(&bar[b], (uint32_t)((consumed / Sh::NBUF) & 1));
+      mbar_wait(&full[b], (uint32_t)((consumed / Sh::NBUF) & 1));
       const double* Bst = sB + b * Sh::STAGE_DBL;
 #pragma unroll
       for (int kk = 0; kk < Sh::KPS; ++kk) {
         const int ks = st * Sh::KPS + kk;
-        double a[4];
-        const double2* ap = reinterpret_cast<const double2*>(&sA[((mt * Sh::KS + ks) * 32 + lane) * 4]);
-        double2 a01 = ap[0], a23 = ap[1];
-        a[0] = a01.x; a[1] = a01.y; a[2] = a23.x; a[3] = a23.y;
-        const double2* bp =
-            reinterpret_cast<const double2*>(&Bst[((kk * Sh::NT + nh * Sh::NTW) * 32 + lane) * 2]);
+        double a[Sh::MT][4];
+#pragma unroll
+        for (int mt = 0; mt < Sh::MT; ++mt) {
+          const double2* ap =
+              reinterpret_cast<const double2*>(&sA[((mt * Sh::KS + ks) * 32 + lane) * 4]);
+          const double2 a01 = ap[0], a23 = ap[1];
+          a[mt][0] = a01.x;
+          a[mt][1] = a01.y;
+          a[mt][2] = a23.x;
+          a[mt][3] = a23.y;
+        }
 #pragma unroll
         for (int i = 0; i < Sh::NTW; ++i) {
-          double2 bv = bp[i * 32];
-          double bb[2] = {bv.x, bv.y};
-          dmma16x8x8(c[i], a, bb);
+          if (i < ntw) {
+            const int ntile = warp + i * Sh::WARPS;
+            const double2 bv =
+                reinterpret_cast<const double2*>(Bst)[(kk * Sh::NT + ntile) * 32 + lane];
+            const double bb[2] = {bv.x, bv.y};
+#pragma unroll
+            for (int mt = 0; mt < Sh::MT; ++mt) dmma16x8x8(c[mt][i], a[mt], bb);
+          }
         }
       }
       ++consumed;
-      __syncthreads();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[b]);
       if (tid == 0 && issued < total_loads) issue(issued++);
     }
 
-    // ---- epilogue: mirror the symmetric half into 16-cell staging, coalesced stores
-    double* stg = sA;  // A region is dead until the next prologue
-#pragma unroll 1
-    for (int r = 0; r < Sh::MT; ++r) {
-      if (mt == r) {
+    // ---- epilogue: mirror the symmetric half into staging, coalesced stores --
+    __syncthreads();  // all warps done reading sA
+    double* stg = sA;
 #pragma unroll
-        for (int i = 0; i < Sh::NTW; ++i) {
+    for (int r = 0; r < Sh::CELLS / Sh::OUTC; ++r) {  // unrolled: static fragment indices
+      const int mt = r >> 1, h = r & 1;  // rows g + 8h of m-tile mt
 #pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            const int row = g + 8 * (v >> 1);
-            const int p = (nh * Sh::NTW + i) * 8 + 2 * t + (v & 1);
+      for (int i = 0; i < Sh::NTW; ++i) {
+        if (i < ntw) {
+          const int ntile = warp + i * Sh::WARPS;
+#pragma unroll
+          for (int vv = 0; vv < 2; ++vv) {
+            const int p = ntile * 8 + 2 * t + vv;
             if (p < Sh::NP) {
+              const double val = h ? c[mt][i][2 + vv] : c[mt][i][vv];
               const int jk = sPair[p];
-              stg[row * NS * NS + (jk & 0xffff)] = c[i][v];
-              stg[row * NS * NS + (jk >> 16)] = c[i][v];
+              stg[g * Sh::RS + (jk & 0xffff)] = val;
+              stg[g * Sh::RS + (jk >> 16)] = val;
             }
           }
         }
       }
       __syncthreads();
-      const long cb = c0 + r * 16;
-      const int ncell = (int)max(0L, min(16L, E - cb));
-      double2* gA = reinterpret_cast<double2*>(A + cb * NS * NS);
-      const double2* s2 = reinterpret_cast<const double2*>(stg);
-      for (int i = tid; i < ncell * NS * NS / 2; i += Sh::THREADS) {
-        double2 v = s2[i];
+      const long cb = c0 + r * Sh::OUTC;
+      const int ncell = (int)max(0L, min((long)Sh::OUTC, E - cb));
+      constexpr int PER = NS * NS / 2;  // double2 per cell
+      for (int i = tid; i < ncell * PER; i += Sh::THREADS) {
+        const int lc = i / PER, w = i % PER;
+        double2 v = *reinterpret_cast<const double2*>(&stg[lc * Sh::RS + 2 * w]);
+        double2* dst = reinterpret_cast<double2*>(A + (cb + lc) * NS * NS) + w;
         if (acc) {
-          double2 o = gA[i];
+          const double2 o = *dst;
           v.x += o.x;
           v.y += o.y;
         }
-        stg_stream(gA + i, v);
+        stg_stream(dst, v);
       }
       __syncthreads();
     }
@@ -320,8 +391,7 @@ __global__ void __launch_bounds__(256, 1)
 
 template <int NS, int NC>
 static cudaError_t launch_tensor_t(long E, const double* coords, const double* coef,
-                                   const double* Sfrag, double* A, int acc, cudaStream_t s,
-                                   int max_ctas) {
+                                   const double* Sfrag, double* A, int acc, cudaStream_t s) {
   using Sh = HelmTensorShape<NS, NC>;
   static bool configured = false;
   if (!configured) {
@@ -331,7 +401,8 @@ static cudaError_t launch_tensor_t(long E, const double* coords, const double* c
     configured = true;
   }
   const long ntiles = (E + Sh::CELLS - 1) / Sh::CELLS;
-  const int grid = (int)(ntiles < (long)max_ctas ? ntiles : (long)max_ctas);
+  const long max_ctas = 2L * kNumSMs;  // persistent: two CTAs per SM
+  const int grid = (int)(ntiles < max_ctas ? ntiles : max_ctas);
   helm_tensor_kernel<NS, NC><<<grid, Sh::THREADS, Sh::SMEM, s>>>(E, coords, coef, Sfrag, A, acc);
   return cudaGetLastError();
 }
@@ -356,10 +427,9 @@ void helm_tensor_geometry(int ns, int nc, int* KS, int* NT, int* KR, int* NP) {
 cudaError_t launch_helm_tensor(int ns, int nc, long E, const double* coords, const double* coef,
                                const double* Sfrag, double* A, int acc, cudaStream_t s) {
   if (E <= 0) return cudaSuccess;
-  const int ctas = kNumSMs;  // persistent: one CTA per SM
-  if (ns == 20 && nc == 20) return launch_tensor_t<20, 20>(E, coords, coef, Sfrag, A, acc, s, ctas);
-  if (ns == 10 && nc == 10) return launch_tensor_t<10, 10>(E, coords, coef, Sfrag, A, acc, s, ctas);
-  if (ns == 10 && nc == 4) return launch_tensor_t<10, 4>(E, coords, coef, Sfrag, A, acc, s, ctas);
+  if (ns == 20 && nc == 20) return launch_tensor_t<20, 20>(E, coords, coef, Sfrag, A, acc, s);
+  if (ns == 10 && nc == 10) return launch_tensor_t<10, 10>(E, coords, coef, Sfrag, A, acc, s);
+  if (ns == 10 && nc == 4) return launch_tensor_t<10, 4>(E, coords, coef, Sfrag, A, acc, s);
   return cudaErrorInvalidValue;
 }
 

@@ -7,21 +7,26 @@
 // "Elasticity per block at Q=8: none pre-evaluated; sharing elimination
 // wins", App. A P13).  Sharing elimination (proj/src/sharing.cpp:409-607)
 // hoists, per quadrature point, the operands that depend on one linear index
-// only; we do the same, cut for the GPU:
+// only; the same structure, cut for the GPU:
 //
-//  * per quadrature point q and basis function j, a record of j-side operands
-//    (elasticity: u_j = mu' g_j, v_j = lam' g_j, g_j;  SVK: s_j = w' S g_j,
-//    lam' h_j, mu' h_j, mu' g_j, g_j, h_j = F g_j), computed once per (cell,j)
-//    instead of once per (j,k) pair;
+//  * per (cell, quadrature point q, basis function j) a record of j-side
+//    operands -- g_j = K^T grad phi_j (elasticity), plus h_j = F g_j and
+//    s_j = w' S g_j (St Venant-Kirchhoff) -- computed once for a chunk of
+//    quadrature points, stored cell-fastest so a half-warp (16 cells, same
+//    (j,k)) reads them conflict-free;
 //  * every (c,d) component block of a (j,k) pair is a rank-2/3 update of these
 //    records (component-blocked vector basis: the zero padding of the FFC
-//    tables, zeroskip.cpp's concept, never enters the arithmetic);
+//    tables, zeroskip.cpp's concept, never enters the arithmetic):
+//      elasticity  A(c,d) += mu' g_j[d] g_k[c] + lam' g_j[c] g_k[d] + d_cd mu' g_j.g_k
+//      SVK         A(c,d) += lam' h_j[c] h_k[d] + mu' h_k[c] h_j[d]
+//                            + mu' (F F^T)_cd g_j.g_k + d_cd s_j.g_k
 //  * A_e is symmetric for both forms: only j<=k pairs are accumulated (2x2
-//    register tiles over the upper triangle), mirrored in the epilogue;
-//  * the records of point q+1 are computed in the same phase as the
-//    accumulation of point q (double buffer), hiding their latency;
-//  * element matrices are staged through shared memory 4 cells at a time and
-//    written with coalesced 16-byte stores.
+//    register tiles over the upper triangle of the 10x10 (j,k) grid), one
+//    (cell, tile) per thread, no synchronisation inside the q loop;
+//  * the 16 element matrices of a tile (115 KB) are staged in shared memory
+//    (cell stride 902 doubles: conflict-free 16-byte stores) and written with
+//    coalesced 16-byte streaming stores; the next tile's inputs are prefetched
+//    with cp.async while the current tile accumulates.
 #include "common.cuh"
 #include "femgpu_internal.h"
 #include "../../include/femgpu.h"
@@ -33,79 +38,96 @@ struct PairShape {
   static constexpr int N = 3 * NS;                       // element matrix N x N
   static constexpr int NJ = NS / 2;                      // 2-wide j/k groups
   static constexpr int NTILE = NJ * (NJ + 1) / 2;        // 2x2 tiles on/above the diagonal
-  static constexpr int CELLS = 16;                       // cells per CTA tile
+  static constexpr int CELLS = 16;                       // cells per CTA tile (= half-warp)
   static constexpr int THREADS = 256;
   static constexpr bool SVK = (KIND == FEMGPU_HYPERELASTICITY);
   static constexpr int NCOEF = SVK ? 3 * NS + 8 : 8;
-  static constexpr int REC = SVK ? 18 : 10;              // j-record doubles
-  // cell stride of a record buffer: (stride/2) odd -> conflict-free LDS.128
-  static constexpr int RS0 = NS * REC + (SVK ? 6 : 0);
-  static constexpr int RSTRIDE = ((RS0 / 2) % 2 == 1) ? RS0 : RS0 + 2;
-  static constexpr int QD = 26;                          // SVK per-(cell,q) scalars
-  static constexpr int TAB = Q + 3 * Q * NS + 4 * Q;     // W | D | P
-  static constexpr int CELLD = 12 + 10 + NCOEF;          // coords | K(9), adet | coeffs
-  static constexpr int OUT_CELLS = 4;                    // epilogue staging round
-  static constexpr int RECBUF = 2 * CELLS * RSTRIDE;
-  static constexpr int STG = OUT_CELLS * N * N;
-  static constexpr int UNION = RECBUF > STG ? RECBUF : STG;
+  static constexpr int QC = SVK ? 9 : Q;                 // quadrature points per chunk
+  static constexpr int NCHUNK = (Q + QC - 1) / QC;
+  static constexpr int RECD = SVK ? 9 : 3;               // per (q,j): g | h | s
+  static constexpr int QSD = SVK ? 8 : 2;                // per q: lam', mu' | F F^T (6)
+  static constexpr int QDD = 18;                         // SVK per (cell,q): F, w'S
+  static constexpr int REC_DBL = QC * (NS * RECD + QSD) * CELLS;
+  static constexpr int CSTRIDE = N * N + 2;              // staging stride: (stride/2) odd
+  static constexpr int STG_DBL = CELLS * CSTRIDE;
+  static constexpr int UNION = REC_DBL > STG_DBL ? REC_DBL : STG_DBL;
+  static constexpr int TAB0 = Q + 3 * Q * NS + 4 * Q;    // W | D | P
+  static constexpr int TAB = (TAB0 + 1) / 2 * 2;
+  static constexpr int CELLD = 12 + 10;                  // coords | K(9), adet
+  static constexpr int IN_DBL = CELLS * (12 + NCOEF);    // raw inputs (cp.async target)
+  static constexpr int QD_DBL = SVK ? QC * CELLS * QDD : 0;
   static constexpr size_t SMEM =
-      sizeof(double) * ((size_t)TAB + CELLS * CELLD + (SVK ? CELLS * Q * QD : 0) + UNION);
+      sizeof(double) * ((size_t)TAB + CELLS * CELLD + IN_DBL + QD_DBL + UNION);
   static_assert(NS % 2 == 0, "2x2 tiling needs an even number of scalar dofs");
-  static_assert(CELLS * NTILE <= THREADS, "one (cell, tile) per thread");
+  static_assert(CELLS * (NTILE + 1) <= THREADS, "one (cell, tile) per thread");
+  static_assert((CSTRIDE / 2) % 2 == 1, "conflict-free staging stride");
 };
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
 
 template <int KIND, int NS, int Q>
 __global__ void __launch_bounds__(256, 1)
     pair_kernel(long E, const double* __restrict__ coords, const double* __restrict__ coef,
                 const double* __restrict__ tab, double* __restrict__ A, int acc) {
   using Sh = PairShape<KIND, NS, Q>;
-  constexpr int N = Sh::N;
+  constexpr int N = Sh::N, CELLS = Sh::CELLS;
   extern __shared__ __align__(16) double smem[];
   double* sW = smem;
-  double* sD = sW + Q;            // [3][Q][NS]
-  double* sP = sD + 3 * Q * NS;   // [Q][4]
-  double* sCell = smem + Sh::TAB; // [CELLS][CELLD]
-  double* sQ = sCell + Sh::CELLS * Sh::CELLD;                 // SVK: [CELLS][Q][QD]
-  double* sU = sQ + (Sh::SVK ? Sh::CELLS * Q * Sh::QD : 0);   // records / staging
+  double* sD = sW + Q;                      // [3][Q][NS]
+  double* sP = sD + 3 * Q * NS;             // [Q][4]
+  double* sCell = smem + Sh::TAB;           // [CELLS][CELLD]
+  double* sIn = sCell + CELLS * Sh::CELLD;  // [CELLS][12] | [CELLS][NCOEF]
+  double* sQd = sIn + Sh::IN_DBL;           // SVK: [QC][CELLS][QDD]
+  double* sU = sQd + Sh::QD_DBL;            // records (chunk) / output staging
+  // record layout: rec[((ql*NS + j)*RECD + comp)*CELLS + cell], then per-q scalars
+  double* sQs = sU + Sh::QC * NS * Sh::RECD * CELLS;  // [QC][QSD][CELLS]
 
   const int tid = threadIdx.x;
-  for (int i = tid; i < Sh::TAB; i += Sh::THREADS) smem[i] = tab[i];
+  for (int i = tid; i < Sh::TAB0; i += Sh::THREADS) smem[i] = tab[i];
 
-  // (cell, tile) owned in the accumulation phase
-  const int my_cell = tid % Sh::CELLS;
-  const int my_tile = tid / Sh::CELLS;
+  const int cell = tid % CELLS;
+  const int my_tile = tid / CELLS;
   const bool active = my_tile < Sh::NTILE;
   int TJ = 0, TK = 0;
   {
     int t = active ? my_tile : 0;
     for (int J = 0; J < Sh::NJ; ++J) {
-      int len = Sh::NJ - J;
-      if (t < len) { TJ = J; TK = J + t; break; }
+      const int len = Sh::NJ - J;
+      if (t < len) {
+        TJ = J;
+        TK = J + t;
+        break;
+      }
       t -= len;
     }
   }
   const int j0 = 2 * TJ, k0 = 2 * TK;
 
-  const long ntiles = (E + Sh::CELLS - 1) / Sh::CELLS;
+  const long ntiles = (E + CELLS - 1) / CELLS;
+  auto prefetch = [&](long tile) {
+    const long c0 = tile * CELLS;
+    const int nt = (int)min((long)CELLS, E - c0);
+    for (int i = tid; i < nt * 12; i += Sh::THREADS) cp_async8(&sIn[i], coords + c0 * 12 + i);
+    for (int i = tid; i < nt * Sh::NCOEF; i += Sh::THREADS)
+      cp_async8(&sIn[CELLS * 12 + i], coef + c0 * Sh::NCOEF + i);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  if ((long)blockIdx.x < ntiles) prefetch(blockIdx.x);
+
   for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const long c0 = tile * Sh::CELLS;
-    const int nt = (int)min((long)Sh::CELLS, E - c0);
-    __syncthreads();  // previous epilogue done with sCell / staging
-    // ---- load raw inputs (coalesced) ---------------------------------------
-    for (int i = tid; i < Sh::CELLS * 12; i += Sh::THREADS) {
-      const int c = i / 12, r = i % 12;
-      // cells past the end get the reference tet (finite geometry, never stored)
-      const double ref = (r == 3 || r == 7 || r == 11) ? 1.0 : 0.0;
-      sCell[c * Sh::CELLD + r] = c < nt ? coords[(c0 + c) * 12 + r] : ref;
-    }
-    for (int i = tid; i < Sh::CELLS * Sh::NCOEF; i += Sh::THREADS) {
-      const int c = i / Sh::NCOEF, r = i % Sh::NCOEF;
-      sCell[c * Sh::CELLD + 22 + r] = c < nt ? coef[(c0 + c) * Sh::NCOEF + r] : 0.0;
-    }
+    const long c0 = tile * CELLS;
+    const int nt = (int)min((long)CELLS, E - c0);
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
     __syncthreads();
-    if (tid < Sh::CELLS) {
+    if (tid < CELLS) {
+      double x[12];
+#pragma unroll
+      for (int r = 0; r < 12; ++r)  // cells past the end: reference tet (never stored)
+        x[r] = tid < nt ? sIn[tid * 12 + r] : ((r == 3 || r == 7 || r == 11) ? 1.0 : 0.0);
+      const Geo g = cell_geometry(x);
       double* cd = sCell + tid * Sh::CELLD;
-      const Geo g = cell_geometry(cd);
 #pragma unroll
       for (int a = 0; a < 3; ++a)
 #pragma unroll
@@ -113,120 +135,8 @@ __global__ void __launch_bounds__(256, 1)
       cd[21] = g.adet;
     }
     __syncthreads();
-    if constexpr (Sh::SVK) {
-      // ---- per (cell, q): F, w' S, F F^T, lam', mu' (St Venant-Kirchhoff) --
-      for (int task = tid; task < Sh::CELLS * Q; task += Sh::THREADS) {
-        const int c = task / Q, q = task % Q;
-        const double* cd = sCell + c * Sh::CELLD;
-        const double* K = cd + 12;
-        const double* w = cd + 22;              // [3][NS]
-        const double* mu = cd + 22 + 3 * NS;
-        const double* lam = mu + 4;
-        double muq = 0, lamq = 0;
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          muq += mu[m] * sP[q * 4 + m];
-          lamq += lam[m] * sP[q * 4 + m];
-        }
-        const double wq = sW[q] * cd[21];
-        double F[3][3];
-#pragma unroll
-        for (int cc = 0; cc < 3; ++cc) {
-          double gr[3] = {0, 0, 0};  // reference gradient of w_cc
-#pragma unroll
-          for (int m = 0; m < NS; ++m) {
-            const double wm = w[cc * NS + m];
-#pragma unroll
-            for (int a = 0; a < 3; ++a) gr[a] += wm * sD[(a * Q + q) * NS + m];
-          }
-#pragma unroll
-          for (int b = 0; b < 3; ++b)
-            F[cc][b] = (cc == b ? 1.0 : 0.0) + gr[0] * K[0 * 3 + b] + gr[1] * K[1 * 3 + b] +
-                       gr[2] * K[2 * 3 + b];
-        }
-        double Ee[3][3];
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-#pragma unroll
-          for (int b = 0; b < 3; ++b) {
-            const double t = F[0][a] * F[0][b] + F[1][a] * F[1][b] + F[2][a] * F[2][b];
-            Ee[a][b] = 0.5 * (a == b ? t - 1.0 : t);
-          }
-        const double trE = Ee[0][0] + Ee[1][1] + Ee[2][2];
-        double* qd = sQ + (c * Q + q) * Sh::QD;
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-#pragma unroll
-          for (int b = 0; b < 3; ++b) {
-            qd[a * 3 + b] = F[a][b];
-            qd[9 + a * 3 + b] = wq * ((a == b ? lamq * trE : 0.0) + 2.0 * muq * Ee[a][b]);
-          }
-        const int ab[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
-#pragma unroll
-        for (int s = 0; s < 6; ++s) {
-          const int a = ab[s][0], b = ab[s][1];
-          qd[18 + s] = F[a][0] * F[b][0] + F[a][1] * F[b][1] + F[a][2] * F[b][2];
-        }
-        qd[24] = lamq * wq;
-        qd[25] = muq * wq;
-      }
-      __syncthreads();
-    }
-
-    // ---- per-(cell, j) records of point q -> buffer q&1 ---------------------
-    auto make_records = [&](int q) {
-      if (tid >= Sh::CELLS * NS) return;
-      const int c = tid / NS, j = tid % NS;
-      const double* cd = sCell + c * Sh::CELLD;
-      const double* K = cd + 12;
-      double* rec = sU + (q & 1) * Sh::CELLS * Sh::RSTRIDE + c * Sh::RSTRIDE + j * Sh::REC;
-      double g[3];
-#pragma unroll
-      for (int b = 0; b < 3; ++b)
-        g[b] = K[0 * 3 + b] * sD[(0 * Q + q) * NS + j] + K[1 * 3 + b] * sD[(1 * Q + q) * NS + j] +
-               K[2 * 3 + b] * sD[(2 * Q + q) * NS + j];
-      if constexpr (!Sh::SVK) {
-        const double* mu = cd + 22;
-        const double* lam = cd + 26;
-        double muq = 0, lamq = 0;
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          muq += mu[m] * sP[q * 4 + m];
-          lamq += lam[m] * sP[q * 4 + m];
-        }
-        const double wq = sW[q] * cd[21];
-        const double mq = muq * wq, lq = lamq * wq;
-        double2* r2 = reinterpret_cast<double2*>(rec);
-        r2[0] = make_double2(mq * g[0], mq * g[1]);
-        r2[1] = make_double2(mq * g[2], lq * g[0]);
-        r2[2] = make_double2(lq * g[1], lq * g[2]);
-        r2[3] = make_double2(g[0], g[1]);
-        rec[8] = g[2];
-      } else {
-        const double* qd = sQ + (c * Q + q) * Sh::QD;
-        double h[3], s[3];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          h[a] = qd[a * 3 + 0] * g[0] + qd[a * 3 + 1] * g[1] + qd[a * 3 + 2] * g[2];
-          s[a] = qd[9 + a * 3 + 0] * g[0] + qd[9 + a * 3 + 1] * g[1] + qd[9 + a * 3 + 2] * g[2];
-        }
-        const double lq = qd[24], mq = qd[25];
-        double2* r2 = reinterpret_cast<double2*>(rec);
-        r2[0] = make_double2(s[0], s[1]);
-        r2[1] = make_double2(s[2], lq * h[0]);
-        r2[2] = make_double2(lq * h[1], lq * h[2]);
-        r2[3] = make_double2(mq * h[0], mq * h[1]);
-        r2[4] = make_double2(mq * h[2], mq * g[0]);
-        r2[5] = make_double2(mq * g[1], mq * g[2]);
-        r2[6] = make_double2(g[0], g[1]);
-        r2[7] = make_double2(g[2], h[0]);
-        r2[8] = make_double2(h[1], h[2]);
-        if (j == 0) {
-          double* ff = sU + (q & 1) * Sh::CELLS * Sh::RSTRIDE + c * Sh::RSTRIDE + NS * Sh::REC;
-#pragma unroll
-          for (int i = 0; i < 6; ++i) ff[i] = qd[18 + i];
-        }
-      }
+    auto coefv = [&](int c, int r) -> double {
+      return c < nt ? sIn[CELLS * 12 + c * Sh::NCOEF + r] : 0.0;
     };
 
     double a4[2][2][3][3];
@@ -239,126 +149,231 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
           for (int d = 0; d < 3; ++d) a4[x][y][c][d] = 0.0;
 
-    make_records(0);
-    __syncthreads();
 #pragma unroll 1
-    for (int q = 0; q < Q; ++q) {
-      if (q + 1 < Q) make_records(q + 1);
+    for (int ch = 0; ch < Sh::NCHUNK; ++ch) {
+      const int q0 = ch * Sh::QC;
+      const int qn = min(Sh::QC, Q - q0);
+      if constexpr (Sh::SVK) {
+        // ---- per (cell, q): F = I + grad w, w' S, F F^T, lam', mu' ---------
+        for (int task = tid; task < CELLS * qn; task += Sh::THREADS) {
+          const int c = task % CELLS, ql = task / CELLS, q = q0 + ql;
+          const double* cd = sCell + c * Sh::CELLD;
+          const double* K = cd + 12;
+          double muq = 0, lamq = 0;
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            muq += coefv(c, 3 * NS + m) * sP[q * 4 + m];
+            lamq += coefv(c, 3 * NS + 4 + m) * sP[q * 4 + m];
+          }
+          const double wq = sW[q] * cd[21];
+          double F[3][3];
+#pragma unroll
+          for (int cc = 0; cc < 3; ++cc) {
+            double gr[3] = {0, 0, 0};  // reference gradient of w_cc
+#pragma unroll
+            for (int m = 0; m < NS; ++m) {
+              const double wm = coefv(c, cc * NS + m);
+#pragma unroll
+              for (int a = 0; a < 3; ++a) gr[a] += wm * sD[(a * Q + q) * NS + m];
+            }
+#pragma unroll
+            for (int b = 0; b < 3; ++b)
+              F[cc][b] = (cc == b ? 1.0 : 0.0) + gr[0] * K[0 * 3 + b] + gr[1] * K[1 * 3 + b] +
+                         gr[2] * K[2 * 3 + b];
+          }
+          double Ee[3][3];
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b) {
+              const double t = F[0][a] * F[0][b] + F[1][a] * F[1][b] + F[2][a] * F[2][b];
+              Ee[a][b] = 0.5 * (a == b ? t - 1.0 : t);
+            }
+          const double trE = Ee[0][0] + Ee[1][1] + Ee[2][2];
+          double* qd = sQd + (ql * CELLS + c) * Sh::QDD;
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b) {
+              qd[a * 3 + b] = F[a][b];
+              qd[9 + a * 3 + b] = wq * ((a == b ? lamq * trE : 0.0) + 2.0 * muq * Ee[a][b]);
+            }
+          double* qs = sQs + ql * Sh::QSD * CELLS + c;
+          qs[0 * CELLS] = lamq * wq;
+          qs[1 * CELLS] = muq * wq;
+          // F F^T: (0,0),(0,1),(0,2),(1,1),(1,2),(2,2)
+          qs[2 * CELLS] = F[0][0] * F[0][0] + F[0][1] * F[0][1] + F[0][2] * F[0][2];
+          qs[3 * CELLS] = F[0][0] * F[1][0] + F[0][1] * F[1][1] + F[0][2] * F[1][2];
+          qs[4 * CELLS] = F[0][0] * F[2][0] + F[0][1] * F[2][1] + F[0][2] * F[2][2];
+          qs[5 * CELLS] = F[1][0] * F[1][0] + F[1][1] * F[1][1] + F[1][2] * F[1][2];
+          qs[6 * CELLS] = F[1][0] * F[2][0] + F[1][1] * F[2][1] + F[1][2] * F[2][2];
+          qs[7 * CELLS] = F[2][0] * F[2][0] + F[2][1] * F[2][1] + F[2][2] * F[2][2];
+        }
+        __syncthreads();
+      }
+      // ---- records of the chunk: per (cell, q, j) -------------------------
+      for (int task = tid; task < CELLS * qn * NS; task += Sh::THREADS) {
+        const int c = task % CELLS, r = task / CELLS;
+        const int j = r % NS, ql = r / NS, q = q0 + ql;
+        const double* cd = sCell + c * Sh::CELLD;
+        const double* K = cd + 12;
+        double g[3];
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+          g[b] = K[0 * 3 + b] * sD[(0 * Q + q) * NS + j] + K[1 * 3 + b] * sD[(1 * Q + q) * NS + j] +
+                 K[2 * 3 + b] * sD[(2 * Q + q) * NS + j];
+        double* rec = sU + ((ql * NS + j) * Sh::RECD) * CELLS + c;
+#pragma unroll
+        for (int b = 0; b < 3; ++b) rec[b * CELLS] = g[b];
+        if constexpr (Sh::SVK) {
+          const double* qd = sQd + (ql * CELLS + c) * Sh::QDD;
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            rec[(3 + a) * CELLS] = qd[a * 3 + 0] * g[0] + qd[a * 3 + 1] * g[1] + qd[a * 3 + 2] * g[2];
+            rec[(6 + a) * CELLS] =
+                qd[9 + a * 3 + 0] * g[0] + qd[9 + a * 3 + 1] * g[1] + qd[9 + a * 3 + 2] * g[2];
+          }
+        } else if (j == 0) {
+          double muq = 0, lamq = 0;
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            muq += coefv(c, m) * sP[q * 4 + m];
+            lamq += coefv(c, 4 + m) * sP[q * 4 + m];
+          }
+          const double wq = sW[q] * cd[21];
+          double* qs = sQs + ql * Sh::QSD * CELLS + c;
+          qs[0] = lamq * wq;
+          qs[CELLS] = muq * wq;
+        }
+      }
+      __syncthreads();
+      if (ch == Sh::NCHUNK - 1 && tile + gridDim.x < ntiles) prefetch(tile + gridDim.x);
+      // ---- accumulate (no synchronisation inside) --------------------------
       if (active) {
-        const double* base = sU + (q & 1) * Sh::CELLS * Sh::RSTRIDE + my_cell * Sh::RSTRIDE;
-        if constexpr (!Sh::SVK) {
+#pragma unroll 1
+        for (int ql = 0; ql < qn; ++ql) {
+          const double* rq = sU + ql * NS * Sh::RECD * CELLS + cell;
+          const double* qs = sQs + ql * Sh::QSD * CELLS + cell;
+          const double lq = qs[0], mq = qs[CELLS];
           double gk[2][3];
 #pragma unroll
-          for (int y = 0; y < 2; ++y) {
-            const double* r = base + (k0 + y) * Sh::REC;
-            const double2 p0 = *reinterpret_cast<const double2*>(r + 6);
-            gk[y][0] = p0.x; gk[y][1] = p0.y; gk[y][2] = r[8];
-          }
+          for (int y = 0; y < 2; ++y)
 #pragma unroll
-          for (int x = 0; x < 2; ++x) {
-            const double* r = base + (j0 + x) * Sh::REC;
-            const double2 p0 = *reinterpret_cast<const double2*>(r);
-            const double2 p1 = *reinterpret_cast<const double2*>(r + 2);
-            const double2 p2 = *reinterpret_cast<const double2*>(r + 4);
-            const double u[3] = {p0.x, p0.y, p1.x}, v[3] = {p1.y, p2.x, p2.y};
+            for (int b = 0; b < 3; ++b) gk[y][b] = rq[((k0 + y) * Sh::RECD + b) * CELLS];
+          if constexpr (!Sh::SVK) {
 #pragma unroll
-            for (int y = 0; y < 2; ++y) {
-              const double S = u[0] * gk[y][0] + u[1] * gk[y][1] + u[2] * gk[y][2];
+            for (int x = 0; x < 2; ++x) {
+              double u[3], v[3];
 #pragma unroll
-              for (int c = 0; c < 3; ++c)
+              for (int b = 0; b < 3; ++b) {
+                const double gj = rq[((j0 + x) * Sh::RECD + b) * CELLS];
+                u[b] = mq * gj;
+                v[b] = lq * gj;
+              }
 #pragma unroll
-                for (int d = 0; d < 3; ++d)
-                  a4[x][y][c][d] = fma(u[d], gk[y][c], fma(v[c], gk[y][d], a4[x][y][c][d]));
+              for (int y = 0; y < 2; ++y) {
+                const double S = u[0] * gk[y][0] + u[1] * gk[y][1] + u[2] * gk[y][2];
 #pragma unroll
-              for (int c = 0; c < 3; ++c) a4[x][y][c][c] += S;
+                for (int c = 0; c < 3; ++c)
+#pragma unroll
+                  for (int d = 0; d < 3; ++d)
+                    a4[x][y][c][d] = fma(u[d], gk[y][c], fma(v[c], gk[y][d], a4[x][y][c][d]));
+#pragma unroll
+                for (int c = 0; c < 3; ++c) a4[x][y][c][c] += S;
+              }
             }
-          }
-        } else {
-          double gk[2][3], hk[2][3];
+          } else {
+            double hk[2][3];
 #pragma unroll
-          for (int y = 0; y < 2; ++y) {
-            const double* r = base + (k0 + y) * Sh::REC;
-            const double2 p0 = *reinterpret_cast<const double2*>(r + 12);
-            const double2 p1 = *reinterpret_cast<const double2*>(r + 14);
-            const double2 p2 = *reinterpret_cast<const double2*>(r + 16);
-            gk[y][0] = p0.x; gk[y][1] = p0.y; gk[y][2] = p1.x;
-            hk[y][0] = p1.y; hk[y][1] = p2.x; hk[y][2] = p2.y;
-          }
-          const double* ffp = base + NS * Sh::REC;
-          const double ff[3][3] = {{ffp[0], ffp[1], ffp[2]}, {ffp[1], ffp[3], ffp[4]},
-                                   {ffp[2], ffp[4], ffp[5]}};
+            for (int y = 0; y < 2; ++y)
 #pragma unroll
-          for (int x = 0; x < 2; ++x) {
-            const double* r = base + (j0 + x) * Sh::REC;
-            double rv[12];
+              for (int b = 0; b < 3; ++b) hk[y][b] = rq[((k0 + y) * Sh::RECD + 3 + b) * CELLS];
+            const double f00 = qs[2 * CELLS], f01 = qs[3 * CELLS], f02 = qs[4 * CELLS];
+            const double f11 = qs[5 * CELLS], f12 = qs[6 * CELLS], f22 = qs[7 * CELLS];
+            const double ff[3][3] = {{f00, f01, f02}, {f01, f11, f12}, {f02, f12, f22}};
 #pragma unroll
-            for (int i = 0; i < 6; ++i) {
-              const double2 p = *reinterpret_cast<const double2*>(r + 2 * i);
-              rv[2 * i] = p.x;
-              rv[2 * i + 1] = p.y;
-            }
-            const double* s = rv;       // w' S g_j
-            const double* lh = rv + 3;  // lam' h_j
-            const double* mh = rv + 6;  // mu' h_j
-            const double* mg = rv + 9;  // mu' g_j
+            for (int x = 0; x < 2; ++x) {
+              double gj[3], lh[3], mh[3], s[3];
 #pragma unroll
-            for (int y = 0; y < 2; ++y) {
-              const double t1 = s[0] * gk[y][0] + s[1] * gk[y][1] + s[2] * gk[y][2];
-              const double t2 = mg[0] * gk[y][0] + mg[1] * gk[y][1] + mg[2] * gk[y][2];
+              for (int b = 0; b < 3; ++b) {
+                const double* r = rq + ((j0 + x) * Sh::RECD) * CELLS;
+                gj[b] = mq * r[b * CELLS];           // mu' g_j
+                const double h = r[(3 + b) * CELLS];
+                lh[b] = lq * h;                      // lam' h_j
+                mh[b] = mq * h;                      // mu' h_j
+                s[b] = r[(6 + b) * CELLS];           // w' S g_j
+              }
 #pragma unroll
-              for (int c = 0; c < 3; ++c)
+              for (int y = 0; y < 2; ++y) {
+                const double t1 = s[0] * gk[y][0] + s[1] * gk[y][1] + s[2] * gk[y][2];
+                const double t2 = gj[0] * gk[y][0] + gj[1] * gk[y][1] + gj[2] * gk[y][2];
 #pragma unroll
-                for (int d = 0; d < 3; ++d)
-                  a4[x][y][c][d] =
-                      fma(lh[c], hk[y][d], fma(hk[y][c], mh[d], fma(t2, ff[c][d], a4[x][y][c][d])));
+                for (int c = 0; c < 3; ++c)
 #pragma unroll
-              for (int c = 0; c < 3; ++c) a4[x][y][c][c] += t1;
+                  for (int d = 0; d < 3; ++d)
+                    a4[x][y][c][d] = fma(lh[c], hk[y][d],
+                                         fma(hk[y][c], mh[d], fma(t2, ff[c][d], a4[x][y][c][d])));
+#pragma unroll
+                for (int c = 0; c < 3; ++c) a4[x][y][c][c] += t1;
+              }
             }
           }
         }
       }
-      __syncthreads();
+      __syncthreads();  // records consumed (next chunk / staging overwrite them)
     }
 
-    // ---- epilogue: mirror into staging, 4 cells per round, coalesced stores --
-    double* stg = sU;
-#pragma unroll 1
-    for (int r = 0; r < Sh::CELLS / Sh::OUT_CELLS; ++r) {
-      const int lc = my_cell - r * Sh::OUT_CELLS;
-      if (active && lc >= 0 && lc < Sh::OUT_CELLS) {
-        double* As = stg + lc * N * N;
+    // ---- epilogue: mirror into staging (all 16 cells), coalesced stores -----
+    double* stg = sU + cell * Sh::CSTRIDE;
+    if (active) {
 #pragma unroll
-        for (int x = 0; x < 2; ++x)
+      for (int x = 0; x < 2; ++x)
 #pragma unroll
-          for (int y = 0; y < 2; ++y) {
-            const int j = j0 + x, k = k0 + y;
-            if (j > k) continue;
+        for (int c = 0; c < 3; ++c)
 #pragma unroll
-            for (int c = 0; c < 3; ++c)
-#pragma unroll
-              for (int d = 0; d < 3; ++d) {
-                const double v = a4[x][y][c][d];
-                As[(c * NS + j) * N + d * NS + k] = v;
-                As[(d * NS + k) * N + c * NS + j] = v;
-              }
+          for (int d = 0; d < 3; ++d) {
+            const int j = j0 + x;
+            // row (c, j), columns (d, k0..k0+1): one 16-byte store
+            *reinterpret_cast<double2*>(&stg[(c * NS + j) * N + d * NS + k0]) =
+                make_double2(a4[x][0][c][d], a4[x][1][c][d]);
           }
+      if (TJ != TK) {
+#pragma unroll
+        for (int y = 0; y < 2; ++y)
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              const int k = k0 + y;
+              // mirror: row (d, k), columns (c, j0..j0+1)
+              *reinterpret_cast<double2*>(&stg[(d * NS + k) * N + c * NS + j0]) =
+                  make_double2(a4[0][y][c][d], a4[1][y][c][d]);
+            }
+      } else {
+        // diagonal tile: entry (j0+1, k0) is the mirror of (j0, k0+1)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int d = 0; d < 3; ++d)
+            stg[(d * NS + k0 + 1) * N + c * NS + j0] = a4[0][1][c][d];
       }
-      __syncthreads();
-      const long cb = c0 + r * Sh::OUT_CELLS;
-      const int ncell = (int)max(0L, min((long)Sh::OUT_CELLS, E - cb));
-      double2* gA = reinterpret_cast<double2*>(A + cb * N * N);
-      const double2* s2 = reinterpret_cast<const double2*>(stg);
-      for (int i = tid; i < ncell * N * N / 2; i += Sh::THREADS) {
-        double2 v = s2[i];
+    }
+    __syncthreads();
+    {
+      const int per = N * N / 2;  // double2 per cell
+      for (int i = tid; i < nt * per; i += Sh::THREADS) {
+        const int c = i / per, w = i % per;
+        double2 v = *reinterpret_cast<const double2*>(&sU[c * Sh::CSTRIDE + 2 * w]);
+        double2* dst = reinterpret_cast<double2*>(A + (c0 + c) * (size_t)N * N) + w;
         if (acc) {
-          double2 o = gA[i];
+          const double2 o = *dst;
           v.x += o.x;
           v.y += o.y;
         }
-        stg_stream(gA + i, v);
+        stg_stream(dst, v);
       }
-      __syncthreads();
     }
+    __syncthreads();
   }
 }
 
@@ -374,7 +389,7 @@ static cudaError_t launch_pair_t(long E, const double* coords, const double* coe
     configured = true;
   }
   const long ntiles = (E + Sh::CELLS - 1) / Sh::CELLS;
-  const int grid = (int)(ntiles < (long)kNumSMs * 8 ? ntiles : (long)kNumSMs * 8);
+  const int grid = (int)(ntiles < (long)kNumSMs ? ntiles : (long)kNumSMs);
   pair_kernel<KIND, NS, Q><<<grid, Sh::THREADS, Sh::SMEM, s>>>(E, coords, coef, tab, A, acc);
   return cudaGetLastError();
 }
