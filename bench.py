@@ -30,7 +30,8 @@ DEFAULT_CONFIG = "c2"  # BASELINE.json configs[1]: the metric's headline config
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=0,
+                    help="timed steps (0 = auto: enough for >= 2 s of timed region)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default=DEFAULT_CONFIG)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -139,9 +140,9 @@ def f_alg(cfg_name):
     """Reference-derived algorithmic flops/cell: min over femopt plans of
     flop_count(optimize(IR)) (tests/golden/<cfg>.json, written by the reference)."""
     try:
-        with open(os.path.join(ROOT, "tests", "golden", f"{cfg_name}.json")) as f:
+        with open(os.path.join(ROOT, "tests", "golden", "falg.json")) as f:
             meta = json.load(f)
-        return min(p["flops_per_cell"] for p in meta["plans"].values())
+        return min(p["flops_per_cell"] for p in meta[cfg_name].values())
     except (OSError, KeyError, ValueError):
         return None
 
@@ -255,15 +256,25 @@ def run_ours(args, rank, world, local):
     def step():
         form.assemble(x, c, out, stream=stream)
 
+    clk = ClockSampler(local).__enter__()  # sample clocks across warm-up and timed region
+    w0 = time.perf_counter()
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize(dev)
+    est_ms = (time.perf_counter() - w0) * 1e3 / max(3, args.warmup)
+    if args.steps <= 0:  # auto: a timed region of >= 2 s (clock samples under load)
+        args.steps = int(max(20, min(5000, 2000.0 / max(est_ms, 1e-3))))
+    t_wait = time.perf_counter()
+    while not clk.lines and time.perf_counter() - t_wait < 3.0:
+        step()
+        torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     per_launch = []
-    with ClockSampler(local) as clk:
+    clk.lines.clear()
+    if True:
         torch.cuda.synchronize(dev)
         ev0.record(stream)
         evs = []
@@ -276,6 +287,7 @@ def run_ours(args, rank, world, local):
             evs.append((a, b))
         ev1.record(stream)
         torch.cuda.synchronize(dev)
+    clk.__exit__(None, None, None)
     total_ms = ev0.elapsed_time(ev1)
     per_launch = [a.elapsed_time(b) for a, b in evs]
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)

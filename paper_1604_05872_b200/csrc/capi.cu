@@ -78,15 +78,23 @@ struct femgpu_form {
   int kernels_per_launch = 1;
   std::string kernel_name;
   std::vector<std::string> argv_out, argv_tab, argv_con;
+  // host-path pipeline resources, created on first use and reused
+  static constexpr int NSTREAM = 3;
+  std::mutex host_mu;
+  cudaStream_t host_st[NSTREAM] = {nullptr, nullptr, nullptr};
+  double* host_buf[NSTREAM] = {nullptr, nullptr, nullptr};
+  long host_chunk = 0;
 
   ~femgpu_form() {
-    if (d_tab) {
-      int cur = 0;
-      cudaGetDevice(&cur);
-      cudaSetDevice(device);
-      cudaFree(d_tab);
-      cudaSetDevice(cur);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(device);
+    if (d_tab) cudaFree(d_tab);
+    for (int i = 0; i < NSTREAM; ++i) {
+      if (host_buf[i]) cudaFree(host_buf[i]);
+      if (host_st[i]) cudaStreamDestroy(host_st[i]);
     }
+    cudaSetDevice(cur);
   }
 };
 
@@ -417,60 +425,57 @@ int femgpu_assemble(const femgpu_form* f, long ncells, const double* coords, con
   });
 }
 
-int femgpu_assemble_host(const femgpu_form* f, long ncells, const double* coords,
+int femgpu_assemble_host(const femgpu_form* fc, long ncells, const double* coords,
                          const double* coeffs, double* A, int accumulate) {
-  if (!f) {
+  if (!fc) {
     g_last_error = "null form";
     return FEMGPU_ERR_INVALID_ARG;
   }
+  femgpu_form* f = const_cast<femgpu_form*>(fc);  // pipeline cache only; guarded below
   return guarded([&] {
     if (ncells < 0) throw Error(FEMGPU_ERR_INVALID_ARG, "negative cell count");
     if (ncells == 0) return;
     if (!coords || !A || (f->ncoef > 0 && !coeffs)) throw Error(FEMGPU_ERR_INVALID_ARG, "null buffer");
+    std::lock_guard<std::mutex> lock(f->host_mu);
     const size_t nn = (size_t)f->n * f->n;
-    // ~64 MiB of element matrices per chunk, multiple of 64 cells
-    long chunk = std::max<long>(64, (long)((64u << 20) / (nn * 8)) / 64 * 64);
-    chunk = std::min(chunk, ncells);
-    const int NSTREAM = 3;
-    cudaStream_t st[NSTREAM];
-    double* dbuf[NSTREAM] = {nullptr, nullptr, nullptr};
+    // ~128 MiB of element matrices per chunk (multiple of 64 cells); three
+    // streams rotate H2D -> kernel -> D2H so both copy engines stay busy.
+    const long chunk = std::max<long>(64, (long)((128u << 20) / (nn * 8)) / 64 * 64);
     const size_t per_cell = 12 + f->ncoef + nn;
-    struct Cleanup {
-      cudaStream_t* st;
-      double** buf;
-      int n;
-      ~Cleanup() {
-        for (int i = 0; i < n; ++i) {
-          if (buf[i]) cudaFree(buf[i]);
-          if (st[i]) cudaStreamDestroy(st[i]);
-        }
+    if (f->host_chunk != chunk) {
+      for (int i = 0; i < femgpu_form::NSTREAM; ++i) {
+        if (!f->host_st[i])
+          cuda_check(cudaStreamCreateWithFlags(&f->host_st[i], cudaStreamNonBlocking),
+                     "cudaStreamCreate");
+        if (f->host_buf[i]) cudaFree(f->host_buf[i]);
+        f->host_buf[i] = nullptr;
+        cuda_check(cudaMalloc(&f->host_buf[i], per_cell * chunk * sizeof(double)),
+                   "cudaMalloc(chunk)");
       }
-    } cleanup{st, dbuf, NSTREAM};
-    for (int i = 0; i < NSTREAM; ++i) st[i] = nullptr;
-    for (int i = 0; i < NSTREAM; ++i) {
-      cuda_check(cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking), "cudaStreamCreate");
-      cuda_check(cudaMalloc(&dbuf[i], per_cell * chunk * sizeof(double)), "cudaMalloc(chunk)");
+      f->host_chunk = chunk;
     }
     long ci = 0;
     for (long c0 = 0; c0 < ncells; c0 += chunk, ++ci) {
       const long E = std::min(chunk, ncells - c0);
-      const int s = (int)(ci % NSTREAM);
-      double* dx = dbuf[s];
+      const int s = (int)(ci % femgpu_form::NSTREAM);
+      cudaStream_t st = f->host_st[s];
+      double* dx = f->host_buf[s];
       double* dA = dx + 12 * chunk;  // 16B aligned: chunk is a multiple of 64
       double* dc = dA + nn * chunk;
       cuda_check(cudaMemcpyAsync(dx, coords + c0 * 12, E * 12 * sizeof(double),
-                                 cudaMemcpyHostToDevice, st[s]), "H2D coords");
+                                 cudaMemcpyHostToDevice, st), "H2D coords");
       if (f->ncoef > 0)
         cuda_check(cudaMemcpyAsync(dc, coeffs + c0 * f->ncoef, E * f->ncoef * sizeof(double),
-                                   cudaMemcpyHostToDevice, st[s]), "H2D coeffs");
+                                   cudaMemcpyHostToDevice, st), "H2D coeffs");
       if (accumulate)
         cuda_check(cudaMemcpyAsync(dA, A + c0 * nn, E * nn * sizeof(double),
-                                   cudaMemcpyHostToDevice, st[s]), "H2D A");
-      launch(f, E, dx, dc, dA, accumulate, st[s]);
+                                   cudaMemcpyHostToDevice, st), "H2D A");
+      launch(f, E, dx, dc, dA, accumulate, st);
       cuda_check(cudaMemcpyAsync(A + c0 * nn, dA, E * nn * sizeof(double), cudaMemcpyDeviceToHost,
-                                 st[s]), "D2H A");
+                                 st), "D2H A");
     }
-    for (int i = 0; i < NSTREAM; ++i) cuda_check(cudaStreamSynchronize(st[i]), "sync");
+    for (int i = 0; i < femgpu_form::NSTREAM; ++i)
+      cuda_check(cudaStreamSynchronize(f->host_st[i]), "sync");
   });
 }
 

@@ -373,16 +373,28 @@ __global__ void __launch_bounds__(256, 2)
       const long cb = c0 + r * Sh::OUTC;
       const int ncell = (int)max(0L, min((long)Sh::OUTC, E - cb));
       constexpr int PER = NS * NS / 2;  // double2 per cell
-      for (int i = tid; i < ncell * PER; i += Sh::THREADS) {
-        const int lc = i / PER, w = i % PER;
-        double2 v = *reinterpret_cast<const double2*>(&stg[lc * Sh::RS + 2 * w]);
-        double2* dst = reinterpret_cast<double2*>(A + (cb + lc) * NS * NS) + w;
-        if (acc) {
-          const double2 o = *dst;
-          v.x += o.x;
-          v.y += o.y;
+      const int total = ncell * PER;
+      double2* gA = reinterpret_cast<double2*>(A + cb * NS * NS);
+      constexpr int U = 4;              // independent loads in flight per thread
+      for (int base = 0; base < total; base += U * Sh::THREADS) {
+        double2 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i = base + u * Sh::THREADS + tid;
+          if (i < total) v[u] = *reinterpret_cast<const double2*>(&stg[(i / PER) * Sh::RS + 2 * (i % PER)]);
         }
-        stg_stream(dst, v);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i = base + u * Sh::THREADS + tid;
+          if (i < total) {
+            if (acc) {
+              const double2 o = gA[i];
+              v[u].x += o.x;
+              v[u].y += o.y;
+            }
+            stg_stream(gA + i, v[u]);
+          }
+        }
       }
       __syncthreads();
     }

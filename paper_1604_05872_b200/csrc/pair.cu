@@ -12,8 +12,8 @@
 //  * per (cell, quadrature point q, basis function j) a record of j-side
 //    operands -- g_j = K^T grad phi_j (elasticity), plus h_j = F g_j and
 //    s_j = w' S g_j (St Venant-Kirchhoff) -- computed once for a chunk of
-//    quadrature points, stored cell-fastest so a half-warp (16 cells, same
-//    (j,k)) reads them conflict-free;
+//    quadrature points, stored cell-fastest so the 8 lanes of one (j,k) tile
+//    read consecutive addresses;
 //  * every (c,d) component block of a (j,k) pair is a rank-2/3 update of these
 //    records (component-blocked vector basis: the zero padding of the FFC
 //    tables, zeroskip.cpp's concept, never enters the arithmetic):
@@ -23,10 +23,11 @@
 //  * A_e is symmetric for both forms: only j<=k pairs are accumulated (2x2
 //    register tiles over the upper triangle of the 10x10 (j,k) grid), one
 //    (cell, tile) per thread, no synchronisation inside the q loop;
-//  * the 16 element matrices of a tile (115 KB) are staged in shared memory
+//  * the 8 element matrices of a tile (58 KB) are staged in shared memory
 //    (cell stride 902 doubles: conflict-free 16-byte stores) and written with
 //    coalesced 16-byte streaming stores; the next tile's inputs are prefetched
-//    with cp.async while the current tile accumulates.
+//    with cp.async while the current tile accumulates; 2-3 CTAs per SM overlap
+//    one tile's store burst with another's arithmetic.
 #include "common.cuh"
 #include "femgpu_internal.h"
 #include "../../include/femgpu.h"
@@ -38,9 +39,10 @@ struct PairShape {
   static constexpr int N = 3 * NS;                       // element matrix N x N
   static constexpr int NJ = NS / 2;                      // 2-wide j/k groups
   static constexpr int NTILE = NJ * (NJ + 1) / 2;        // 2x2 tiles on/above the diagonal
-  static constexpr int CELLS = 16;                       // cells per CTA tile (= half-warp)
-  static constexpr int THREADS = 256;
+  static constexpr int CELLS = 8;                        // cells per CTA tile
+  static constexpr int THREADS = 128;                    // 8 cells x 16 tile slots
   static constexpr bool SVK = (KIND == FEMGPU_HYPERELASTICITY);
+  static constexpr int CTAS_PER_SM = SVK ? 2 : 3;        // independent tiles overlap phases
   static constexpr int NCOEF = SVK ? 3 * NS + 8 : 8;
   static constexpr int QC = SVK ? 9 : Q;                 // quadrature points per chunk
   static constexpr int NCHUNK = (Q + QC - 1) / QC;
@@ -68,7 +70,7 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
 }
 
 template <int KIND, int NS, int Q>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(128, PairShape<KIND, NS, Q>::CTAS_PER_SM)
     pair_kernel(long E, const double* __restrict__ coords, const double* __restrict__ coef,
                 const double* __restrict__ tab, double* __restrict__ A, int acc) {
   using Sh = PairShape<KIND, NS, Q>;
@@ -360,17 +362,30 @@ __global__ void __launch_bounds__(256, 1)
     }
     __syncthreads();
     {
-      const int per = N * N / 2;  // double2 per cell
-      for (int i = tid; i < nt * per; i += Sh::THREADS) {
-        const int c = i / per, w = i % per;
-        double2 v = *reinterpret_cast<const double2*>(&sU[c * Sh::CSTRIDE + 2 * w]);
-        double2* dst = reinterpret_cast<double2*>(A + (c0 + c) * (size_t)N * N) + w;
-        if (acc) {
-          const double2 o = *dst;
-          v.x += o.x;
-          v.y += o.y;
+      constexpr int PER = N * N / 2;  // double2 per cell
+      const int total = nt * PER;
+      double2* gA = reinterpret_cast<double2*>(A + c0 * (size_t)N * N);
+      constexpr int U = 4;            // independent loads in flight per thread
+      for (int base = 0; base < total; base += U * Sh::THREADS) {
+        double2 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i = base + u * Sh::THREADS + tid;
+          if (i < total)
+            v[u] = *reinterpret_cast<const double2*>(&sU[(i / PER) * Sh::CSTRIDE + 2 * (i % PER)]);
         }
-        stg_stream(dst, v);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i = base + u * Sh::THREADS + tid;
+          if (i < total) {
+            if (acc) {
+              const double2 o = gA[i];
+              v[u].x += o.x;
+              v[u].y += o.y;
+            }
+            stg_stream(gA + i, v[u]);
+          }
+        }
       }
     }
     __syncthreads();
@@ -389,7 +404,8 @@ static cudaError_t launch_pair_t(long E, const double* coords, const double* coe
     configured = true;
   }
   const long ntiles = (E + Sh::CELLS - 1) / Sh::CELLS;
-  const int grid = (int)(ntiles < (long)kNumSMs ? ntiles : (long)kNumSMs);
+  const long maxc = (long)Sh::CTAS_PER_SM * kNumSMs;
+  const int grid = (int)(ntiles < maxc ? ntiles : maxc);
   pair_kernel<KIND, NS, Q><<<grid, Sh::THREADS, Sh::SMEM, s>>>(E, coords, coef, tab, A, acc);
   return cudaGetLastError();
 }
