@@ -233,7 +233,8 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
       // ---- GEMM-1 per component c, then direct + mirror stores ------------
-#pragma unroll 1
+      // (unrolled: the delta_cd selection of C is resolved at compile time)
+#pragma unroll
       for (int c = 0; c < 3; ++c) {
         double hacc[3][2][4];
 #pragma unroll

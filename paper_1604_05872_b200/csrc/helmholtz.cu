@@ -40,9 +40,10 @@ constexpr int P1_IN = P1_TILE * 16;                       // doubles per input s
 constexpr size_t P1_SMEM = sizeof(double) * (P1_NBUF * P1_IN + P1_TILE * P1_SO) +
                            P1_NBUF * sizeof(uint64_t);
 
+template <bool ACC>
 __global__ void __launch_bounds__(P1_TILE, P1_CTAS)
     helm_p1_kernel(HelmP1Params prm, long E, const double* __restrict__ coords,
-                   const double* __restrict__ coef, double* __restrict__ A, int acc) {
+                   const double* __restrict__ coef, double* __restrict__ A) {
   extern __shared__ __align__(16) double smem[];
   double* sIn = smem;                               // [NBUF][coords 128x12 | f 128x4]
   double* so = smem + P1_NBUF * P1_IN;              // [128][18]
@@ -119,16 +120,25 @@ __global__ void __launch_bounds__(P1_TILE, P1_CTAS)
       if (nx < ntiles) issue(nx, b);
     }
     double2* gA = reinterpret_cast<double2*>(A + e0 * 16);
-    for (int i = tid; i < nt * 8; i += P1_TILE) {
-      double2 v = *reinterpret_cast<const double2*>(&so[(i / 8) * P1_SO + 2 * (i % 8)]);
-      if (acc) {
-        const double2 o = gA[i];
-        v.x += o.x;
-        v.y += o.y;
-      }
-      stg_stream(gA + i, v);
+    double2 v[8];  // all 8 staged loads in flight before the streaming stores
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = u * P1_TILE + tid;
+      if (i < nt * 8) v[u] = *reinterpret_cast<const double2*>(&so[(i / 8) * P1_SO + 2 * (i % 8)]);
     }
     __syncthreads();  // staging free for the next tile
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = u * P1_TILE + tid;
+      if (i < nt * 8) {
+        if (ACC) {
+          const double2 o = gA[i];
+          v[u].x += o.x;
+          v[u].y += o.y;
+        }
+        stg_stream(gA + i, v[u]);
+      }
+    }
   }
 }
 
@@ -137,21 +147,32 @@ cudaError_t launch_helm_p1(const HelmP1Params& prm, long E, const double* coords
   if (E <= 0) return cudaSuccess;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(helm_p1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)P1_SMEM);
-    if (e != cudaSuccess) return e;
+    for (auto fn : {helm_p1_kernel<false>, helm_p1_kernel<true>}) {
+      cudaError_t e =
+          cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P1_SMEM);
+      if (e != cudaSuccess) return e;
+    }
     configured = true;
   }
   const long ntiles = (E + P1_TILE - 1) / P1_TILE;
   const long maxc = (long)P1_CTAS * kNumSMs;
   const int grid = (int)(ntiles < maxc ? ntiles : maxc);
-  helm_p1_kernel<<<grid, P1_TILE, P1_SMEM, s>>>(prm, E, coords, coef, A, acc);
+  if (acc)
+    helm_p1_kernel<true><<<grid, P1_TILE, P1_SMEM, s>>>(prm, E, coords, coef, A);
+  else
+    helm_p1_kernel<false><<<grid, P1_TILE, P1_SMEM, s>>>(prm, E, coords, coef, A);
   return cudaGetLastError();
 }
 
 // ============================================================================
-// Tensor schedule on the FP64 tensor cores
+// Tensor schedule on the FP64 tensor cores -- warp-specialised, persistent
 // ============================================================================
+//   warps 0..7   MMA: C[32 cells x 8*NT] += g (smem) x S (TMA ring), then drop
+//                the symmetric half (j<=k) into a 32-cell staging tile
+//   warps 8..10  IO:  inputs -> per-cell factors g (fragment-native, double
+//                buffered) for the NEXT tile; mirrored, coalesced copy-out
+//   warp  11     TMA producer: S k-chunks into a 3-stage ring (bulk copies)
+// so the tensor cores never wait for a prologue or an epilogue.
 template <int NS, int NC>
 struct HelmTensorShape {
   static constexpr int NP = NS * (NS + 1) / 2;          // symmetric half of A_e
@@ -160,243 +181,266 @@ struct HelmTensorShape {
   static constexpr int KPS = 2;                         // k8 steps per pipeline stage
   static constexpr int KS = ((KR + 8 * KPS - 1) / (8 * KPS)) * KPS;  // k8 steps (padded)
   static constexpr int NSTG = KS / KPS;                 // stages per tile
-  static constexpr int NBUF = 2;                        // pipeline depth
-  static constexpr int MT = 2;                          // m16 tiles per CTA
-  static constexpr int CELLS = 16 * MT;                 // cells per CTA tile
-  static constexpr int THREADS = 256;                   // 8 warps, n-tiles interleaved
-  static constexpr int WARPS = THREADS / 32;
-  static constexpr int NTW = (NT + WARPS - 1) / WARPS;  // max n8 tiles per warp
-  static constexpr int STAGE_DBL = KPS * NT * 64;       // doubles per B stage
+  static constexpr int NBUF = 3;                        // TMA ring depth
+  static constexpr int MT = 2;                          // m16 tiles per CTA tile
+  static constexpr int CELLS = 16 * MT;                 // cells per tile
+  static constexpr int MMA_WARPS = 8;
+  static constexpr int IO_WARPS = 3;
+  static constexpr int IO_THREADS = 32 * IO_WARPS;
+  static constexpr int THREADS = 32 * (MMA_WARPS + IO_WARPS + 1);
+  static constexpr int NTW = (NT + MMA_WARPS - 1) / MMA_WARPS;  // max n8 tiles per MMA warp
+  static constexpr int STAGE_DBL = KPS * NT * 64;       // doubles per ring stage
   static constexpr int A_DBL = MT * KS * 128;           // fragment-native g tile
   static constexpr int IN_DBL = CELLS * (12 + NC);      // raw inputs of a tile
-  static constexpr int RS = NS * NS + 6;                // staging row stride (fewer conflicts)
-  static constexpr int OUTC = 8;                        // cells per epilogue round
-  static_assert(OUTC * RS <= A_DBL, "epilogue staging must fit in the A region");
-  static constexpr size_t SMEM = sizeof(double) * (size_t)(A_DBL + NBUF * STAGE_DBL + IN_DBL) +
-                                 2 * NBUF * sizeof(uint64_t) + NP * sizeof(int);
+  static constexpr int SP = NP + 2;                     // staging row: symmetric half only
+  static constexpr int STG_DBL = CELLS * SP;
+  static constexpr int NBAR = 2 * NBUF + 4 + 2;
+  static constexpr size_t SMEM =
+      sizeof(double) * (size_t)(2 * A_DBL + NBUF * STAGE_DBL + IN_DBL + STG_DBL) +
+      NBAR * sizeof(uint64_t) + NS * NS * sizeof(short);
 };
 
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.wait_all;\n" ::: "memory");
-}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
+__device__ __forceinline__ void io_barrier(int nthreads) {
+  asm volatile("bar.sync 1, %0;\n" ::"r"(nthreads) : "memory");
+}
 
 template <int NS, int NC>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(HelmTensorShape<NS, NC>::THREADS, 1)
     helm_tensor_kernel(long E, const double* __restrict__ coords, const double* __restrict__ coef,
                        const double* __restrict__ Sfrag, double* __restrict__ A, int acc) {
   using Sh = HelmTensorShape<NS, NC>;
   extern __shared__ __align__(16) double smem[];
-  double* sA = smem;                                  // [MT][KS][32][4]
-  double* sB = sA + Sh::A_DBL;                        // [NBUF][KPS][NT][32][2]
-  double* sIn = sB + Sh::NBUF * Sh::STAGE_DBL;        // [CELLS][12] then [CELLS][NC]
-  uint64_t* full = reinterpret_cast<uint64_t*>(sIn + Sh::IN_DBL);
-  uint64_t* empty = full + Sh::NBUF;
-  int* sPair = reinterpret_cast<int*>(empty + Sh::NBUF);  // p -> (j*NS+k) | (k*NS+j) << 16
+  double* sA = smem;                                  // [2][MT][KS][32][4]
+  double* sB = sA + 2 * Sh::A_DBL;                    // [NBUF][KPS][NT][32][2]
+  double* sIn = sB + Sh::NBUF * Sh::STAGE_DBL;        // [CELLS][12] | [CELLS][NC]
+  double* stg = sIn + Sh::IN_DBL;                     // [CELLS][SP] (j<=k half)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(stg + Sh::STG_DBL);
+  uint64_t* bFull = bar;                              // [NBUF]  TMA -> MMA
+  uint64_t* bEmpty = bar + Sh::NBUF;                  // [NBUF]  MMA -> producer
+  uint64_t* aFull = bar + 2 * Sh::NBUF;               // [2]     IO -> MMA
+  uint64_t* aEmpty = aFull + 2;                       // [2]     MMA -> IO
+  uint64_t* sFull = aFull + 4;                        //         MMA -> IO (staging written)
+  uint64_t* sEmpty = aFull + 5;                       //         IO -> MMA (staging drained)
+  short* sPidx = reinterpret_cast<short*>(bar + Sh::NBAR);  // (j,k) -> p(min, max)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t = lane & 3;
   const long ntiles = (E + Sh::CELLS - 1) / Sh::CELLS;
   if ((long)blockIdx.x >= ntiles) return;
+  const long my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
 
   if (tid == 0) {
     for (int b = 0; b < Sh::NBUF; ++b) {
-      mbar_init(&full[b], 1);
-      mbar_init(&empty[b], Sh::WARPS);
+      mbar_init(&bFull[b], 1);
+      mbar_init(&bEmpty[b], Sh::MMA_WARPS);
     }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&aFull[b], Sh::IO_THREADS);
+      mbar_init(&aEmpty[b], Sh::MMA_WARPS);
+    }
+    mbar_init(sFull, Sh::MMA_WARPS);
+    mbar_init(sEmpty, Sh::IO_THREADS);
     fence_mbar_init();
   }
-  for (int j = 0, p = 0; j < NS; ++j)
-    for (int k = j; k < NS; ++k, ++p)
-      if (p % Sh::THREADS == tid) sPair[p] = (j * NS + k) | ((k * NS + j) << 16);
+  for (int jk = tid; jk < NS * NS; jk += Sh::THREADS) {
+    const int j = jk / NS, k = jk % NS;
+    const int lo = j < k ? j : k, hi = j < k ? k : j;
+    sPidx[jk] = (short)(lo * NS - lo * (lo - 1) / 2 + (hi - lo));
+  }
   __syncthreads();
 
-  // B pipeline: loads numbered globally, load i carries k-chunk i % NSTG into
-  // buffer i % NBUF.  full[b]: TMA transaction count; empty[b]: one arrival per
-  // warp once it has consumed the buffer.  Never leave a copy in flight at exit.
-  const long my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
-  const long total_loads = my_tiles * Sh::NSTG;
-  long issued = 0;
-  auto issue = [&](long i) {
-    const int b = (int)(i % Sh::NBUF);
-    if (i >= Sh::NBUF) mbar_wait(&empty[b], (uint32_t)(((i / Sh::NBUF) - 1) & 1));
-    const int chunk = (int)(i % Sh::NSTG);
-    mbar_expect_tx(&full[b], Sh::STAGE_DBL * 8);
-    bulk_g2s(sB + b * Sh::STAGE_DBL, Sfrag + (size_t)chunk * Sh::STAGE_DBL, Sh::STAGE_DBL * 8,
-             &full[b]);
-  };
-  if (tid == 0)
-    for (; issued < Sh::NBUF && issued < total_loads; ++issued) issue(issued);
-  long consumed = 0;
-
-  auto load_inputs = [&](long tile) {
-    const long c0 = tile * Sh::CELLS;
-    const int nt = (int)min((long)Sh::CELLS, E - c0);
-    for (int i = tid; i < nt * 12; i += Sh::THREADS) cp_async8(&sIn[i], coords + c0 * 12 + i);
-    for (int i = tid; i < nt * NC; i += Sh::THREADS)
-      cp_async8(&sIn[Sh::CELLS * 12 + i], coef + c0 * NC + i);
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-  };
-  load_inputs(blockIdx.x);
-
-  // n-tiles of this warp: warp, warp+8, ... (balanced across the 4 SM sub-partitions)
-  int ntw = 0;
-  for (int nt_ = warp; nt_ < Sh::NT; nt_ += Sh::WARPS) ++ntw;
-
-  for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const long c0 = tile * Sh::CELLS;
-    const int nt = (int)min((long)Sh::CELLS, E - c0);
-    cp_async_wait_all();
-    __syncthreads();
-    // ---- prologue: g[cell][alpha] -> sA (fragment-native), 8 threads per cell
-    {
-      const int cell = tid >> 3, part = tid & 7;
-      constexpr int MPT = (NC + 7) / 8;
-      double Gs[7];
-      double fv[MPT];
-      if (cell < nt) {
-        const Geo geo = cell_geometry(&sIn[cell * 12]);
-        const double(*K)[3] = geo.K;
+  if (warp < Sh::MMA_WARPS) {
+    // ======================= MMA warps =======================
+    const int g = lane >> 2, t = lane & 3;
+    int ntw = 0;
+    for (int x = warp; x < Sh::NT; x += Sh::MMA_WARPS) ++ntw;
+    long consumed = 0;
+    for (long it = 0; it < my_tiles; ++it) {
+      const int ab = (int)(it & 1);
+      mbar_wait(&aFull[ab], (uint32_t)((it >> 1) & 1));
+      const double* sAb = sA + ab * Sh::A_DBL;
+      double c[Sh::MT][Sh::NTW][4];
 #pragma unroll
-        for (int s = 0; s < 6; ++s) {
-          const int a = s < 3 ? s : (s == 5 ? 1 : 0);
-          const int b = s < 3 ? s : (s == 3 ? 1 : 2);
-          Gs[s] = geo.adet * (K[a][0] * K[b][0] + K[a][1] * K[b][1] + K[a][2] * K[b][2]);
-        }
-        Gs[6] = geo.adet;
+      for (int mt = 0; mt < Sh::MT; ++mt)
 #pragma unroll
-        for (int i = 0; i < MPT; ++i) {
-          const int m = part + 8 * i;
-          fv[i] = m < NC ? sIn[Sh::CELLS * 12 + cell * NC + m] : 0.0;
-        }
-      } else {
+        for (int i = 0; i < Sh::NTW; ++i) c[mt][i][0] = c[mt][i][1] = c[mt][i][2] = c[mt][i][3] = 0.0;
+#pragma unroll 1
+      for (int st = 0; st < Sh::NSTG; ++st) {
+        const int b = (int)(consumed % Sh::NBUF);
+        mbar_wait(&bFull[b], (uint32_t)((consumed / Sh::NBUF) & 1));
+        const double* Bst = sB + b * Sh::STAGE_DBL;
 #pragma unroll
-        for (int s = 0; s < 7; ++s) Gs[s] = 0.0;
+        for (int kk = 0; kk < Sh::KPS; ++kk) {
+          const int ks = st * Sh::KPS + kk;
+          double a[Sh::MT][4];
 #pragma unroll
-        for (int i = 0; i < MPT; ++i) fv[i] = 0.0;
-      }
-      const int cmt = cell >> 4, rr = cell & 15;
-      const int gg = rr & 7, vrow = rr >> 3;
+          for (int mt = 0; mt < Sh::MT; ++mt) {
+            const double2* ap =
+                reinterpret_cast<const double2*>(&sAb[((mt * Sh::KS + ks) * 32 + lane) * 4]);
+            const double2 a01 = ap[0], a23 = ap[1];
+            a[mt][0] = a01.x;
+            a[mt][1] = a01.y;
+            a[mt][2] = a23.x;
+            a[mt][3] = a23.y;
+          }
 #pragma unroll
-      for (int i = 0; i < MPT; ++i) {
-        const int m = part + 8 * i;
-        if (m < NC) {
+          for (int i = 0; i < Sh::NTW; ++i) {
+            if (i < ntw) {
+              const int ntile = warp + i * Sh::MMA_WARPS;
+              const double2 bv =
+                  reinterpret_cast<const double2*>(Bst)[(kk * Sh::NT + ntile) * 32 + lane];
+              const double bb[2] = {bv.x, bv.y};
 #pragma unroll
-          for (int s = 0; s < 7; ++s) {
-            const int alpha = m * 7 + s;
-            const int ks = alpha >> 3, kk = alpha & 7;
-            const int ln = gg * 4 + (kk & 3), v = vrow + 2 * (kk >> 2);
-            sA[((cmt * Sh::KS + ks) * 32 + ln) * 4 + v] = fv[i] * Gs[s];
+              for (int mt = 0; mt < Sh::MT; ++mt) dmma16x8x8(c[mt][i], a[mt], bb);
+            }
           }
         }
+        ++consumed;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bEmpty[b]);
       }
-      for (int alpha = Sh::KR + part; alpha < 8 * Sh::KS; alpha += 8) {  // zero K padding
-        const int ks = alpha >> 3, kk = alpha & 7;
-        const int ln = gg * 4 + (kk & 3), v = vrow + 2 * (kk >> 2);
-        sA[((cmt * Sh::KS + ks) * 32 + ln) * 4 + v] = 0.0;
-      }
-    }
-    __syncthreads();
-    if (tile + gridDim.x < ntiles) load_inputs(tile + gridDim.x);
-
-    // ---- main loop: every warp computes all MT m-tiles x its n-tiles ---------
-    double c[Sh::MT][Sh::NTW][4];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&aEmpty[ab]);
+      // epilogue: the j<=k half of the tile into staging (the IO warps mirror it)
+      mbar_wait(sEmpty, (uint32_t)(it & 1));
 #pragma unroll
-    for (int mt = 0; mt < Sh::MT; ++mt)
-#pragma unroll
-      for (int i = 0; i < Sh::NTW; ++i) c[mt][i][0] = c[mt][i][1] = c[mt][i][2] = c[mt][i][3] = 0.0;
-#pragma unroll 1
-    for (int st = 0; st < Sh::NSTG; ++st) {
-      const int b = (int)(consumed % Sh::NBUF);
-      mbar_wait(&full[b], (uint32_t)((consumed / Sh::NBUF) & 1));
-      const double* Bst = sB + b * Sh::STAGE_DBL;
-#pragma unroll
-      for (int kk = 0; kk < Sh::KPS; ++kk) {
-        const int ks = st * Sh::KPS + kk;
-        double a[Sh::MT][4];
-#pragma unroll
-        for (int mt = 0; mt < Sh::MT; ++mt) {
-          const double2* ap =
-              reinterpret_cast<const double2*>(&sA[((mt * Sh::KS + ks) * 32 + lane) * 4]);
-          const double2 a01 = ap[0], a23 = ap[1];
-          a[mt][0] = a01.x;
-          a[mt][1] = a01.y;
-          a[mt][2] = a23.x;
-          a[mt][3] = a23.y;
-        }
+      for (int mt = 0; mt < Sh::MT; ++mt)
 #pragma unroll
         for (int i = 0; i < Sh::NTW; ++i) {
           if (i < ntw) {
-            const int ntile = warp + i * Sh::WARPS;
-            const double2 bv =
-                reinterpret_cast<const double2*>(Bst)[(kk * Sh::NT + ntile) * 32 + lane];
-            const double bb[2] = {bv.x, bv.y};
+            const int ntile = warp + i * Sh::MMA_WARPS;
 #pragma unroll
-            for (int mt = 0; mt < Sh::MT; ++mt) dmma16x8x8(c[mt][i], a[mt], bb);
+            for (int v = 0; v < 4; ++v) {
+              const int row = 16 * mt + g + 8 * (v >> 1);
+              const int p = ntile * 8 + 2 * t + (v & 1);
+              if (p < Sh::NP) stg[row * Sh::SP + p] = c[mt][i][v];
+            }
           }
         }
-      }
-      ++consumed;
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[b]);
-      if (tid == 0 && issued < total_loads) issue(issued++);
+      if (lane == 0) mbar_arrive(sFull);
     }
-
-    // ---- epilogue: mirror the symmetric half into staging, coalesced stores --
-    __syncthreads();  // all warps done reading sA
-    double* stg = sA;
+  } else if (warp < Sh::MMA_WARPS + Sh::IO_WARPS) {
+    // ======================= IO warps =======================
+    const int io = tid - 32 * Sh::MMA_WARPS;
+    mbar_arrive(sEmpty);  // staging starts empty (completes phase 0)
+    auto prologue = [&](long it) {
+      const long tile = blockIdx.x + it * gridDim.x;
+      const long c0 = tile * Sh::CELLS;
+      const int nt = (int)min((long)Sh::CELLS, E - c0);
+      const int ab = (int)(it & 1);
+      if (it >= 2) mbar_wait(&aEmpty[ab], (uint32_t)(((it >> 1) - 1) & 1));
+      for (int i = io; i < nt * 12; i += Sh::IO_THREADS) cp_async8(&sIn[i], coords + c0 * 12 + i);
+      for (int i = io; i < nt * NC; i += Sh::IO_THREADS)
+        cp_async8(&sIn[Sh::CELLS * 12 + i], coef + c0 * NC + i);
+      asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::: "memory");
+      io_barrier(Sh::IO_THREADS);
+      double* sAb = sA + ab * Sh::A_DBL;
+      constexpr int PARTS = Sh::IO_THREADS / Sh::CELLS;  // threads per cell
+      constexpr int MPT = (NC + PARTS - 1) / PARTS;
+      const int cell = io / PARTS, part = io % PARTS;
+      if (cell < Sh::CELLS) {
+        double Gs[7];
+        double fv[MPT];
+        if (cell < nt) {
+          const Geo geo = cell_geometry(&sIn[cell * 12]);
+          const double(*K)[3] = geo.K;
 #pragma unroll
-    for (int r = 0; r < Sh::CELLS / Sh::OUTC; ++r) {  // unrolled: static fragment indices
-      const int mt = r >> 1, h = r & 1;  // rows g + 8h of m-tile mt
+          for (int s = 0; s < 6; ++s) {
+            const int a = s < 3 ? s : (s == 5 ? 1 : 0);
+            const int b = s < 3 ? s : (s == 3 ? 1 : 2);
+            Gs[s] = geo.adet * (K[a][0] * K[b][0] + K[a][1] * K[b][1] + K[a][2] * K[b][2]);
+          }
+          Gs[6] = geo.adet;
 #pragma unroll
-      for (int i = 0; i < Sh::NTW; ++i) {
-        if (i < ntw) {
-          const int ntile = warp + i * Sh::WARPS;
+          for (int i = 0; i < MPT; ++i) {
+            const int m = part + PARTS * i;
+            fv[i] = m < NC ? sIn[Sh::CELLS * 12 + cell * NC + m] : 0.0;
+          }
+        } else {
 #pragma unroll
-          for (int vv = 0; vv < 2; ++vv) {
-            const int p = ntile * 8 + 2 * t + vv;
-            if (p < Sh::NP) {
-              const double val = h ? c[mt][i][2 + vv] : c[mt][i][vv];
-              const int jk = sPair[p];
-              stg[g * Sh::RS + (jk & 0xffff)] = val;
-              stg[g * Sh::RS + (jk >> 16)] = val;
+          for (int s = 0; s < 7; ++s) Gs[s] = 0.0;
+#pragma unroll
+          for (int i = 0; i < MPT; ++i) fv[i] = 0.0;
+        }
+        const int cmt = cell >> 4, rr = cell & 15;
+        const int gg = rr & 7, vrow = rr >> 3;
+#pragma unroll
+        for (int i = 0; i < MPT; ++i) {
+          const int m = part + PARTS * i;
+          if (m < NC) {
+#pragma unroll
+            for (int s = 0; s < 7; ++s) {
+              const int alpha = m * 7 + s;
+              const int ks = alpha >> 3, kk = alpha & 7;
+              const int ln = gg * 4 + (kk & 3), v = vrow + 2 * (kk >> 2);
+              sAb[((cmt * Sh::KS + ks) * 32 + ln) * 4 + v] = fv[i] * Gs[s];
             }
           }
         }
-      }
-      __syncthreads();
-      const long cb = c0 + r * Sh::OUTC;
-      const int ncell = (int)max(0L, min((long)Sh::OUTC, E - cb));
-      constexpr int PER = NS * NS / 2;  // double2 per cell
-      const int total = ncell * PER;
-      double2* gA = reinterpret_cast<double2*>(A + cb * NS * NS);
-      constexpr int U = 4;              // independent loads in flight per thread
-      for (int base = 0; base < total; base += U * Sh::THREADS) {
-        double2 v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int i = base + u * Sh::THREADS + tid;
-          if (i < total) v[u] = *reinterpret_cast<const double2*>(&stg[(i / PER) * Sh::RS + 2 * (i % PER)]);
+        for (int alpha = Sh::KR + part; alpha < 8 * Sh::KS; alpha += PARTS) {  // zero K padding
+          const int ks = alpha >> 3, kk = alpha & 7;
+          const int ln = gg * 4 + (kk & 3), v = vrow + 2 * (kk >> 2);
+          sAb[((cmt * Sh::KS + ks) * 32 + ln) * 4 + v] = 0.0;
         }
+      }
+      io_barrier(Sh::IO_THREADS);  // sIn free for the next prologue
+      mbar_arrive(&aFull[ab]);
+    };
+    prologue(0);
+    for (long it = 0; it < my_tiles; ++it) {
+      if (it + 1 < my_tiles) prologue(it + 1);
+      const long c0 = (blockIdx.x + it * gridDim.x) * Sh::CELLS;
+      {
+        mbar_wait(sFull, (uint32_t)(it & 1));
+        const long cb = c0;
+        const int ncell = (int)min((long)Sh::CELLS, E - cb);
+        constexpr int PER = NS * NS / 2;  // double2 per cell
+        const int total = ncell * PER;
+        double2* gA = reinterpret_cast<double2*>(A + cb * NS * NS);
+        constexpr int U = 4;
+        for (int base = 0; base < total; base += U * Sh::IO_THREADS) {
+          double2 v[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int i = base + u * Sh::THREADS + tid;
-          if (i < total) {
-            if (acc) {
-              const double2 o = gA[i];
-              v[u].x += o.x;
-              v[u].y += o.y;
+          for (int u = 0; u < U; ++u) {
+            const int i = base + u * Sh::IO_THREADS + io;
+            if (i < total) {  // mirror: A[j][k] = A[k][j] = staged p(min, max)
+              const double* row = stg + (i / PER) * Sh::SP;
+              const int jk = 2 * (i % PER);
+              v[u] = make_double2(row[sPidx[jk]], row[sPidx[jk + 1]]);
             }
-            stg_stream(gA + i, v[u]);
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int i = base + u * Sh::IO_THREADS + io;
+            if (i < total) {
+              if (acc) {
+                const double2 o = gA[i];
+                v[u].x += o.x;
+                v[u].y += o.y;
+              }
+              stg_stream(gA + i, v[u]);
+            }
           }
         }
+        mbar_arrive(sEmpty);
       }
-      __syncthreads();
+    }
+  } else if (lane == 0) {
+    // ======================= TMA producer =======================
+    const long total_loads = my_tiles * Sh::NSTG;
+    for (long i = 0; i < total_loads; ++i) {
+      const int b = (int)(i % Sh::NBUF);
+      if (i >= Sh::NBUF) mbar_wait(&bEmpty[b], (uint32_t)(((i / Sh::NBUF) - 1) & 1));
+      const int chunk = (int)(i % Sh::NSTG);
+      mbar_expect_tx(&bFull[b], Sh::STAGE_DBL * 8);
+      bulk_g2s(sB + b * Sh::STAGE_DBL, Sfrag + (size_t)chunk * Sh::STAGE_DBL, Sh::STAGE_DBL * 8,
+               &bFull[b]);
     }
   }
 }
@@ -413,7 +457,7 @@ static cudaError_t launch_tensor_t(long E, const double* coords, const double* c
     configured = true;
   }
   const long ntiles = (E + Sh::CELLS - 1) / Sh::CELLS;
-  const long max_ctas = 2L * kNumSMs;  // persistent: two CTAs per SM
+  const long max_ctas = kNumSMs;  // persistent: one warp-specialised CTA per SM
   const int grid = (int)(ntiles < max_ctas ? ntiles : max_ctas);
   helm_tensor_kernel<NS, NC><<<grid, Sh::THREADS, Sh::SMEM, s>>>(E, coords, coef, Sfrag, A, acc);
   return cudaGetLastError();
