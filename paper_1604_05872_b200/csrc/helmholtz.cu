@@ -169,9 +169,9 @@ cudaError_t launch_helm_p1(const HelmP1Params& prm, long E, const double* coords
 // ============================================================================
 //   warps 0..7   MMA: C[32 cells x 8*NT] += g (smem) x S (TMA ring), then drop
 //                the symmetric half (j<=k) into a 32-cell staging tile
-//   warps 8..10  IO:  inputs -> per-cell factors g (fragment-native, double
+//   warps 8..11  IO:  inputs -> per-cell factors g (fragment-native, double
 //                buffered) for the NEXT tile; mirrored, coalesced copy-out
-//   warp  11     TMA producer: S k-chunks into a 3-stage ring (bulk copies)
+//   warp  12     TMA producer: S k-chunks into a 3-stage ring (bulk copies)
 // so the tensor cores never wait for a prologue or an epilogue.
 template <int NS, int NC>
 struct HelmTensorShape {
@@ -185,7 +185,7 @@ struct HelmTensorShape {
   static constexpr int MT = 2;                          // m16 tiles per CTA tile
   static constexpr int CELLS = 16 * MT;                 // cells per tile
   static constexpr int MMA_WARPS = 8;
-  static constexpr int IO_WARPS = 3;
+  static constexpr int IO_WARPS = 4;
   static constexpr int IO_THREADS = 32 * IO_WARPS;
   static constexpr int THREADS = 32 * (MMA_WARPS + IO_WARPS + 1);
   static constexpr int NTW = (NT + MMA_WARPS - 1) / MMA_WARPS;  // max n8 tiles per MMA warp
@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(HelmTensorShape<NS, NC>::THREADS, 1)
     const int g = lane >> 2, t = lane & 3;
     int ntw = 0;
     for (int x = warp; x < Sh::NT; x += Sh::MMA_WARPS) ++ntw;
-    long consumed = 0;
+    int cb_buf = 0, cb_phase = 0;  // ring position of the next stage to consume
     for (long it = 0; it < my_tiles; ++it) {
       const int ab = (int)(it & 1);
       mbar_wait(&aFull[ab], (uint32_t)((it >> 1) & 1));
@@ -271,8 +271,8 @@ __global__ void __launch_bounds__(HelmTensorShape<NS, NC>::THREADS, 1)
         for (int i = 0; i < Sh::NTW; ++i) c[mt][i][0] = c[mt][i][1] = c[mt][i][2] = c[mt][i][3] = 0.0;
 #pragma unroll 1
       for (int st = 0; st < Sh::NSTG; ++st) {
-        const int b = (int)(consumed % Sh::NBUF);
-        mbar_wait(&bFull[b], (uint32_t)((consumed / Sh::NBUF) & 1));
+        const int b = cb_buf;
+        mbar_wait(&bFull[b], (uint32_t)cb_phase);
         const double* Bst = sB + b * Sh::STAGE_DBL;
 #pragma unroll
         for (int kk = 0; kk < Sh::KPS; ++kk) {
@@ -300,7 +300,10 @@ __global__ void __launch_bounds__(HelmTensorShape<NS, NC>::THREADS, 1)
             }
           }
         }
-        ++consumed;
+        if (++cb_buf == Sh::NBUF) {
+          cb_buf = 0;
+          cb_phase ^= 1;
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(&bEmpty[b]);
       }

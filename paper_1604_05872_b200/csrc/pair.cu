@@ -24,8 +24,10 @@
 //    register tiles over the upper triangle of the 10x10 (j,k) grid), one
 //    (cell, tile) per thread, no synchronisation inside the q loop;
 //  * the 8 element matrices of a tile (58 KB) are staged in shared memory
-//    (cell stride 902 doubles: conflict-free 16-byte stores) and written with
-//    coalesced 16-byte streaming stores; the next tile's inputs are prefetched
+//    (cell stride 902 doubles: conflict-free 16-byte stores) and written to HBM
+//    by TMA bulk copies (cp.async.bulk / cp.reduce.async.bulk .add.f64 for the
+//    += contract), so no thread spends time on the store stream; the next
+//    tile's inputs are prefetched
 //    with cp.async while the current tile accumulates; 2-3 CTAs per SM overlap
 //    one tile's store burst with another's arithmetic.
 #include "common.cuh"
@@ -122,6 +124,7 @@ __global__ void __launch_bounds__(128, PairShape<KIND, NS, Q>::CTAS_PER_SM)
     const long c0 = tile * CELLS;
     const int nt = (int)min((long)CELLS, E - c0);
     asm volatile("cp.async.wait_all;\n" ::: "memory");
+    if (tid == 0) bulk_wait_read0();  // previous tile's bulk stores have read the staging
     __syncthreads();
     if (tid < CELLS) {
       double x[12];
@@ -272,14 +275,22 @@ __global__ void __launch_bounds__(128, PairShape<KIND, NS, Q>::CTAS_PER_SM)
                 u[b] = mq * gj;
                 v[b] = lq * gj;
               }
+              // independent FMA passes (no dependent pairs back to back)
 #pragma unroll
-              for (int y = 0; y < 2; ++y) {
-                const double S = u[0] * gk[y][0] + u[1] * gk[y][1] + u[2] * gk[y][2];
+              for (int y = 0; y < 2; ++y)
 #pragma unroll
                 for (int c = 0; c < 3; ++c)
 #pragma unroll
-                  for (int d = 0; d < 3; ++d)
-                    a4[x][y][c][d] = fma(u[d], gk[y][c], fma(v[c], gk[y][d], a4[x][y][c][d]));
+                  for (int d = 0; d < 3; ++d) a4[x][y][c][d] = fma(v[c], gk[y][d], a4[x][y][c][d]);
+#pragma unroll
+              for (int y = 0; y < 2; ++y)
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+#pragma unroll
+                  for (int d = 0; d < 3; ++d) a4[x][y][c][d] = fma(u[d], gk[y][c], a4[x][y][c][d]);
+#pragma unroll
+              for (int y = 0; y < 2; ++y) {
+                const double S = u[0] * gk[y][0] + u[1] * gk[y][1] + u[2] * gk[y][2];
 #pragma unroll
                 for (int c = 0; c < 3; ++c) a4[x][y][c][c] += S;
               }
@@ -305,19 +316,35 @@ __global__ void __launch_bounds__(128, PairShape<KIND, NS, Q>::CTAS_PER_SM)
                 mh[b] = mq * h;                      // mu' h_j
                 s[b] = r[(6 + b) * CELLS];           // w' S g_j
               }
+              double t1[2], t2[2];
 #pragma unroll
               for (int y = 0; y < 2; ++y) {
-                const double t1 = s[0] * gk[y][0] + s[1] * gk[y][1] + s[2] * gk[y][2];
-                const double t2 = gj[0] * gk[y][0] + gj[1] * gk[y][1] + gj[2] * gk[y][2];
+                t1[y] = s[0] * gk[y][0] + s[1] * gk[y][1] + s[2] * gk[y][2];
+                t2[y] = gj[0] * gk[y][0] + gj[1] * gk[y][1] + gj[2] * gk[y][2];
+              }
+              // independent FMA passes over the 18 accumulators of this j
+#pragma unroll
+              for (int y = 0; y < 2; ++y)
 #pragma unroll
                 for (int c = 0; c < 3; ++c)
 #pragma unroll
-                  for (int d = 0; d < 3; ++d)
-                    a4[x][y][c][d] = fma(lh[c], hk[y][d],
-                                         fma(hk[y][c], mh[d], fma(t2, ff[c][d], a4[x][y][c][d])));
+                  for (int d = 0; d < 3; ++d) a4[x][y][c][d] = fma(lh[c], hk[y][d], a4[x][y][c][d]);
 #pragma unroll
-                for (int c = 0; c < 3; ++c) a4[x][y][c][c] += t1;
-              }
+              for (int y = 0; y < 2; ++y)
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+#pragma unroll
+                  for (int d = 0; d < 3; ++d) a4[x][y][c][d] = fma(hk[y][c], mh[d], a4[x][y][c][d]);
+#pragma unroll
+              for (int y = 0; y < 2; ++y)
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+#pragma unroll
+                  for (int d = 0; d < 3; ++d) a4[x][y][c][d] = fma(t2[y], ff[c][d], a4[x][y][c][d]);
+#pragma unroll
+              for (int y = 0; y < 2; ++y)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) a4[x][y][c][c] += t1[y];
             }
           }
         }
@@ -360,36 +387,22 @@ __global__ void __launch_bounds__(128, PairShape<KIND, NS, Q>::CTAS_PER_SM)
             stg[(d * NS + k0 + 1) * N + c * NS + j0] = a4[0][1][c][d];
       }
     }
+    // staged element matrices -> global by the TMA engine (async bulk copies,
+    // or bulk reductions for the += contract); threads move on immediately
+    fence_proxy_async();
     __syncthreads();
-    {
-      constexpr int PER = N * N / 2;  // double2 per cell
-      const int total = nt * PER;
-      double2* gA = reinterpret_cast<double2*>(A + c0 * (size_t)N * N);
-      constexpr int U = 4;            // independent loads in flight per thread
-      for (int base = 0; base < total; base += U * Sh::THREADS) {
-        double2 v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int i = base + u * Sh::THREADS + tid;
-          if (i < total)
-            v[u] = *reinterpret_cast<const double2*>(&sU[(i / PER) * Sh::CSTRIDE + 2 * (i % PER)]);
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int i = base + u * Sh::THREADS + tid;
-          if (i < total) {
-            if (acc) {
-              const double2 o = gA[i];
-              v[u].x += o.x;
-              v[u].y += o.y;
-            }
-            stg_stream(gA + i, v[u]);
-          }
-        }
+    if (tid == 0) {
+      for (int c = 0; c < nt; ++c) {
+        double* dst = A + (c0 + c) * (size_t)N * N;
+        if (acc)
+          bulk_s2g_add(dst, sU + c * Sh::CSTRIDE, N * N * 8);
+        else
+          bulk_s2g(dst, sU + c * Sh::CSTRIDE, N * N * 8);
       }
+      bulk_commit();
     }
-    __syncthreads();
   }
+  if (tid == 0) bulk_wait0();
 }
 
 template <int KIND, int NS, int Q>
