@@ -18,7 +18,7 @@
 //         alpha = (n,a): |det| sum_b u_{b,n} K_ab  x  sum_q W phi_n phi_j D_a(phi_k)
 //                 s:     |det| nu (K K^T)_s       x  sum_q W D_a phi_j D_b phi_k (+ sym)
 //                 mass:  |det| / dt               x  sum_q W phi_j phi_k
-//         (B fragments streamed from L2 straight into registers)
+//         (B fragments through a 4-deep TMA bulk-copy ring, mbarrier full/empty)
 //
 // Output layout without staging: the 20x20 (j,k) plane is cut into 4x4
 // blocks; a warp owns whole upper blocks (J<=K).  An n8 fragment covers two
@@ -38,7 +38,9 @@ constexpr int N = 60;
 constexpr int NBU = 15;            // upper 4x4 blocks (J <= K) of the 20x20 (j,k) plane
 constexpr int NT1 = 3 * NBU * 2;   // GEMM-1 n8 tiles: (a, upper block, half)
 constexpr int KS1 = 5;             // GEMM-1 k4 steps (n = 0..19)
-constexpr int KS2 = 17;            // GEMM-2 k4 steps: 60 (n,a) + 6 (G) + 1 (mass) + pad
+constexpr int KS2 = 18;            // GEMM-2 k4 steps: 60 (n,a) + 6 (G) + 1 (mass) + pad
+constexpr int KPS2 = 3;            // k4 steps per ring stage
+constexpr int NST2 = KS2 / KPS2;   // ring stages per pass
 constexpr int NT2 = 50;            // GEMM-2 n8 tiles: 15 direct + 10 mirror blocks, x2 halves
 constexpr int CELLS = 16;
 constexpr int THREADS = 256;
@@ -49,8 +51,16 @@ constexpr int A1_DBL = 3 * KS1 * 64;           // u_c fragments
 constexpr int A2_DBL = KS2 * 64;               // g2 fragments
 constexpr int IN_DBL = CELLS * (12 + 3 * NS);  // coords | u (cp.async target)
 constexpr int CELLD = 10;                      // K(9), adet
-constexpr size_t SMEM =
-    sizeof(double) * (size_t)(T1_DBL + A1_DBL + A2_DBL + IN_DBL + CELLS * CELLD);
+// GEMM-2 B operand: TMA ring of per-k-step stages.  A tile runs two passes (the
+// first and second block of every warp); pass p's stage holds only the n8
+// tiles its warps need (30 resp. 20), laid out contiguously on the host.
+constexpr int NB = 3;                          // ring depth
+constexpr int SLOTS0 = 30, SLOTS1 = 20;
+constexpr int STAGE_MAX = KPS2 * SLOTS0 * 32;  // doubles
+constexpr int R2_OFF1 = KS2 * SLOTS0 * 32;     // pass-1 offset inside the R2 table
+constexpr size_t SMEM = sizeof(double) * (size_t)(T1_DBL + A1_DBL + A2_DBL + IN_DBL +
+                                                  CELLS * CELLD + NB * STAGE_MAX) +
+                        2 * NB * sizeof(uint64_t);
 }  // namespace bz
 
 // Upper block u (row-major over J <= K) -> (J, K).
@@ -66,9 +76,28 @@ __host__ __device__ constexpr int bz_mirror_slot(int u) {
 }
 
 // Warp work lists (upper blocks), balanced for GEMM-1 + GEMM-2 cost per SM
-// sub-partition (warps w and w+4 share one).
+// sub-partition (warps w and w+4 share one).  Warp 7 (one block only) doubles
+// as the TMA producer of the GEMM-2 ring.
+constexpr int kWblk[bz::WARPS][2] = {{0, 5}, {1, 9}, {2, 12}, {3, 14}, {4, 6},
+                                     {7, 8}, {10, 11}, {13, -1}};
 __constant__ int c_wblk[bz::WARPS][2] = {{0, 5}, {1, 9}, {2, 12}, {3, 14}, {4, 6},
                                          {7, 8}, {10, 11}, {13, -1}};
+// first GEMM-2 slot of warp w in pass p (direct h0, h1, then mirror h0, h1)
+constexpr int bz_slot_base(int w, int p) {
+  int off = 0;
+  for (int x = 0; x < w; ++x) {
+    const int ub = kWblk[x][p];
+    if (ub >= 0) off += (bz_J(ub) == bz_K(ub)) ? 2 : 4;
+  }
+  return off;
+}
+__constant__ int c_slot[bz::WARPS][2] = {
+    {bz_slot_base(0, 0), bz_slot_base(0, 1)}, {bz_slot_base(1, 0), bz_slot_base(1, 1)},
+    {bz_slot_base(2, 0), bz_slot_base(2, 1)}, {bz_slot_base(3, 0), bz_slot_base(3, 1)},
+    {bz_slot_base(4, 0), bz_slot_base(4, 1)}, {bz_slot_base(5, 0), bz_slot_base(5, 1)},
+    {bz_slot_base(6, 0), bz_slot_base(6, 1)}, {bz_slot_base(7, 0), bz_slot_base(7, 1)}};
+static_assert(bz_slot_base(bz::WARPS, 0) == bz::SLOTS0, "pass-0 slot count");
+static_assert(bz_slot_base(bz::WARPS, 1) == bz::SLOTS1, "pass-1 slot count");
 
 __device__ __forceinline__ void dmma16x8x4(double (&c)[4], double a0, double a1, double b) {
   asm volatile(
@@ -88,6 +117,10 @@ __device__ __forceinline__ void cp_async8b(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive_cta_bz(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ void stg64(double* p, double v) {
   asm volatile("st.global.cs.f64 [%0], %1;\n" ::"l"(p), "d"(v) : "memory");
 }
@@ -103,7 +136,10 @@ __global__ void __launch_bounds__(256, 1)
   double* sA2 = sA1 + A1_DBL;           // [KS2][32][2]
   double* sIn = sA2 + A2_DBL;           // [CELLS][12] | [CELLS][60]
   double* sCell = sIn + IN_DBL;         // [CELLS][10]
-  const double* gR2 = tab + T1_DBL;     // [KS2][NT2][32]
+  double* sRing = sCell + CELLS * CELLD;  // [NB][STAGE_MAX]  GEMM-2 B stages
+  uint64_t* rFull = reinterpret_cast<uint64_t*>(sRing + NB * STAGE_MAX);
+  uint64_t* rEmpty = rFull + NB;
+  const double* gR2 = tab + T1_DBL;     // [pass][KS2][slots][32]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -112,6 +148,41 @@ __global__ void __launch_bounds__(256, 1)
     reinterpret_cast<double2*>(sT1)[i] = reinterpret_cast<const double2*>(tab)[i];
 
   const long ntiles = (E + CELLS - 1) / CELLS;
+  const long my_tiles =
+      (long)blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const long total_stages = my_tiles * 2 * NST2;
+  const bool producer = (warp == WARPS - 1) && lane == 0;
+  auto issue_stage = [&](long gs) {  // stage gs -> ring slot gs % NB
+    const int b = (int)(gs % NB);
+    const int pass = (int)((gs / NST2) & 1), st = (int)(gs % NST2);
+    const int slots = pass ? SLOTS1 : SLOTS0;
+    const double* src = gR2 + (pass ? R2_OFF1 : 0) + (size_t)st * KPS2 * slots * 32;
+    mbar_expect_tx(&rFull[b], KPS2 * slots * 32 * 8);
+    bulk_g2s(sRing + b * STAGE_MAX, src, KPS2 * slots * 32 * 8, &rFull[b]);
+  };
+  if (tid == 0) {
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(&rFull[b], 1);
+      mbar_init(&rEmpty[b], WARPS);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (producer)
+    for (long gs = 0; gs < NB && gs < total_stages; ++gs) issue_stage(gs);
+  // consume stage gs (wait full), release it, and (producer) refill the slot
+  auto stage_wait = [&](long gs) {
+    mbar_wait(&rFull[gs % NB], (uint32_t)((gs / NB) & 1));
+  };
+  auto stage_release = [&](long gs) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive_cta_bz(&rEmpty[gs % NB]);
+    if (producer && gs + NB < total_stages) {
+      mbar_wait(&rEmpty[gs % NB], (uint32_t)((gs / NB) & 1));
+      issue_stage(gs + NB);
+    }
+  };
+  long it = -1;
   auto prefetch = [&](long tile) {
     const long c0 = tile * CELLS;
     const int nt = (int)min((long)CELLS, E - c0);
@@ -123,6 +194,7 @@ __global__ void __launch_bounds__(256, 1)
   if ((long)blockIdx.x < ntiles) prefetch(blockIdx.x);
 
   for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    ++it;
     const long c0 = tile * CELLS;
     const int nt = (int)min((long)CELLS, E - c0);
     asm volatile("cp.async.wait_all;\n" ::: "memory");
@@ -189,7 +261,15 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll 1
     for (int wb = 0; wb < 2; ++wb) {
       const int ub = c_wblk[warp][wb];
-      if (ub < 0) break;
+      const long gs0 = (it * 2 + wb) * NST2;  // first ring stage of this pass
+      if (ub < 0) {  // no block in this pass: keep the ring moving
+#pragma unroll 1
+        for (int st = 0; st < NST2; ++st) {
+          stage_wait(gs0 + st);
+          stage_release(gs0 + st);
+        }
+        continue;
+      }
       const int J = bz_J(ub), K = bz_K(ub);
       const int ms = bz_mirror_slot(ub);
       const bool mirror = ms >= 0;
@@ -200,35 +280,33 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
         for (int v = 0; v < 4; ++v) cdir[h][v] = cmir[h][v] = 0.0;
       {
-        const int td = 2 * ub, tm = 30 + 2 * (mirror ? ms : 0);
-        double b0[4] = {0, 0, 0, 0}, b1[4] = {0, 0, 0, 0};
-        auto loadB = [&](int ks, double (&b)[4]) {
-          if (ks >= KS2) return;
-          const double* base = gR2 + (size_t)ks * NT2 * 32 + lane;
-          b[0] = ldg_nc(base + (td + 0) * 32);
-          b[1] = ldg_nc(base + (td + 1) * 32);
-          if (mirror) {
-            b[2] = ldg_nc(base + (tm + 0) * 32);
-            b[3] = ldg_nc(base + (tm + 1) * 32);
-          }
-        };
-        auto step = [&](int ks, const double (&b)[4]) {
-          const double2 a = reinterpret_cast<const double2*>(sA2)[ks * 32 + lane];
-          dmma16x8x4(cdir[0], a.x, a.y, b[0]);
-          dmma16x8x4(cdir[1], a.x, a.y, b[1]);
-          if (mirror) {
-            dmma16x8x4(cmir[0], a.x, a.y, b[2]);
-            dmma16x8x4(cmir[1], a.x, a.y, b[3]);
-          }
-        };
-        loadB(0, b0);
+        const int slot = c_slot[warp][wb];
+        const int slots = wb ? SLOTS1 : SLOTS0;
 #pragma unroll 1
-        for (int ks = 0; ks < KS2; ks += 2) {
-          loadB(ks + 1, b1);
-          step(ks, b0);
-          if (ks + 1 < KS2) {
-            loadB(ks + 2, b0);
-            step(ks + 1, b1);
+        for (int st = 0; st < NST2; ++st) {
+          const long gs = gs0 + st;
+          stage_wait(gs);
+          const double* stb = sRing + (gs % NB) * STAGE_MAX + slot * 32 + lane;
+          double bq[KPS2][4];
+          double2 aq[KPS2];
+#pragma unroll
+          for (int kk = 0; kk < KPS2; ++kk) {  // all operand loads of the stage first
+            const double* p = stb + kk * slots * 32;
+            bq[kk][0] = p[0];
+            bq[kk][1] = p[32];
+            bq[kk][2] = mirror ? p[64] : 0.0;
+            bq[kk][3] = mirror ? p[96] : 0.0;
+            aq[kk] = reinterpret_cast<const double2*>(sA2)[(st * KPS2 + kk) * 32 + lane];
+          }
+          stage_release(gs);
+#pragma unroll
+          for (int kk = 0; kk < KPS2; ++kk) {
+            dmma16x8x4(cdir[0], aq[kk].x, aq[kk].y, bq[kk][0]);
+            dmma16x8x4(cdir[1], aq[kk].x, aq[kk].y, bq[kk][1]);
+            if (mirror) {
+              dmma16x8x4(cmir[0], aq[kk].x, aq[kk].y, bq[kk][2]);
+              dmma16x8x4(cmir[1], aq[kk].x, aq[kk].y, bq[kk][3]);
+            }
           }
         }
       }
@@ -359,21 +437,29 @@ void burgers_tables(int nq, const double* W, const double* B, const double* D, d
         }
         R2[al][j][k] = s;
       }
+  // [pass][ks][slot][32]: warp w's slots of pass p start at bz_slot_base(w, p)
   double* r2 = out + T1_DBL;
-  for (int ub = 0; ub < NBU; ++ub) {
-    const int ms = bz_mirror_slot(ub);
-    for (int h = 0; h < 2; ++h)
-      for (int ks = 0; ks < KS2; ++ks)
-        for (int lane = 0; lane < 32; ++lane) {
-          const int g = lane >> 2, t = lane & 3;
-          int j, k;
-          jk_of(ub, h, g, &j, &k);
-          const int al = ks * 4 + t;
-          // direct tile: C[j][k]
-          r2[((size_t)ks * NT2 + 2 * ub + h) * 32 + lane] = R2[al][j][k];
-          // mirror tile: the lane that writes position (k, j) needs C[k][j]
-          if (ms >= 0) r2[((size_t)ks * NT2 + 30 + 2 * ms + h) * 32 + lane] = R2[al][k][j];
-        }
+  for (int p = 0; p < 2; ++p) {
+    const int slots = p ? SLOTS1 : SLOTS0;
+    double* base = r2 + (p ? R2_OFF1 : 0);
+    for (int w = 0; w < WARPS; ++w) {
+      const int ub = kWblk[w][p];
+      if (ub < 0) continue;
+      const bool off = bz_J(ub) != bz_K(ub);
+      const int s0 = bz_slot_base(w, p);
+      for (int h = 0; h < 2; ++h)
+        for (int ks = 0; ks < KS2; ++ks)
+          for (int lane = 0; lane < 32; ++lane) {
+            const int g = lane >> 2, t = lane & 3;
+            int j, k;
+            jk_of(ub, h, g, &j, &k);
+            const int al = ks * 4 + t;
+            // direct tile: C[j][k]
+            base[((size_t)ks * slots + s0 + h) * 32 + lane] = R2[al][j][k];
+            // mirror tile: the lane that writes position (k, j) needs C[k][j]
+            if (off) base[((size_t)ks * slots + s0 + 2 + h) * 32 + lane] = R2[al][k][j];
+          }
+    }
   }
 }
 

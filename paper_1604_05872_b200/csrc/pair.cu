@@ -11,9 +11,10 @@
 //
 //  * per (cell, quadrature point q, basis function j) a record of j-side
 //    operands -- g_j = K^T grad phi_j (elasticity), plus h_j = F g_j and
-//    s_j = w' S g_j (St Venant-Kirchhoff) -- computed once for a chunk of
-//    quadrature points, stored cell-fastest so the 8 lanes of one (j,k) tile
-//    read consecutive addresses;
+//    s_j = w' S g_j (St Venant-Kirchhoff) -- computed once per chunk of
+//    quadrature points, stored cell-fastest (lanes of one (j,k) tile read
+//    consecutive addresses; j-stride padded so neighbouring tiles of a warp
+//    hit alternate bank halves);
 //  * every (c,d) component block of a (j,k) pair is a rank-2/3 update of these
 //    records (component-blocked vector basis: the zero padding of the FFC
 //    tables, zeroskip.cpp's concept, never enters the arithmetic):
@@ -22,14 +23,20 @@
 //                            + mu' (F F^T)_cd g_j.g_k + d_cd s_j.g_k
 //  * A_e is symmetric for both forms: only j<=k pairs are accumulated (2x2
 //    register tiles over the upper triangle of the 10x10 (j,k) grid), one
-//    (cell, tile) per thread, no synchronisation inside the q loop;
-//  * the 8 element matrices of a tile (58 KB) are staged in shared memory
-//    (cell stride 902 doubles: conflict-free 16-byte stores) and written to HBM
-//    by TMA bulk copies (cp.async.bulk / cp.reduce.async.bulk .add.f64 for the
-//    += contract), so no thread spends time on the store stream; the next
-//    tile's inputs are prefetched
-//    with cp.async while the current tile accumulates; 2-3 CTAs per SM overlap
-//    one tile's store burst with another's arithmetic.
+//    (cell, tile) per accumulating thread, independent FMA passes;
+//  * element matrices are staged in shared memory (cell stride 902 doubles:
+//    conflict-free 16-byte stores) and written by TMA bulk copies
+//    (cp.async.bulk, or cp.reduce.async.bulk .add.f64 for the += contract).
+//
+// Two CTA organisations (chosen per form by measurement, profiles/):
+//  * pair_ws_kernel  (elasticity): warp-specialised -- 2 producer warps build
+//    the records of the next tile into a double buffer (mbarrier full/empty)
+//    while 4 consumer warps accumulate; 2 CTAs per SM;
+//  * pair_flat_kernel (SVK): every thread takes part in each phase (per-point
+//    tensors, records, accumulation); 2 CTAs per SM overlap one CTA's
+//    latency-bound setup with the other's FMA stream.  (A producer/consumer
+//    split was measured slower here: the per-point F, E, S work is ~20% of
+//    the FLOPs and too latency-bound for a minority of warps.)
 #include "common.cuh"
 #include "femgpu_internal.h"
 #include "../../include/femgpu.h"
@@ -38,76 +45,377 @@ namespace femgpu {
 
 template <int KIND, int NS, int Q>
 struct PairShape {
+  static constexpr bool SVK = (KIND == FEMGPU_HYPERELASTICITY);
   static constexpr int N = 3 * NS;                       // element matrix N x N
   static constexpr int NJ = NS / 2;                      // 2-wide j/k groups
   static constexpr int NTILE = NJ * (NJ + 1) / 2;        // 2x2 tiles on/above the diagonal
   static constexpr int CELLS = 8;                        // cells per CTA tile
-  static constexpr int THREADS = 128;                    // 8 cells x 16 tile slots
-  static constexpr bool SVK = (KIND == FEMGPU_HYPERELASTICITY);
-  static constexpr int CTAS_PER_SM = SVK ? 2 : 3;        // independent tiles overlap phases
+  static constexpr int ACC = 128;                        // accumulating threads: 8 x 16 slots
+  static constexpr int PROD = SVK ? 0 : 64;              // producer threads (ws kernel only)
+  static constexpr int THREADS = ACC + PROD;
+  static constexpr int CTAS_PER_SM = 2;
   static constexpr int NCOEF = SVK ? 3 * NS + 8 : 8;
   static constexpr int QC = SVK ? 9 : Q;                 // quadrature points per chunk
   static constexpr int NCHUNK = (Q + QC - 1) / QC;
   static constexpr int RECD = SVK ? 9 : 3;               // per (q,j): g | h | s
   static constexpr int QSD = SVK ? 8 : 2;                // per q: lam', mu' | F F^T (6)
   static constexpr int QDD = 18;                         // SVK per (cell,q): F, w'S
-  static constexpr int REC_DBL = QC * (NS * RECD + QSD) * CELLS;
+  // j-stride of a record buffer: RECD*CELLS + 4 doubles, so the k-side loads of the
+  // (j,k) tiles sharing a warp (k0 two apart) fall in alternate bank halves
+  static constexpr int JS = RECD * CELLS + 4;
+  static constexpr int REC_DBL = QC * (NS * JS + QSD * CELLS);  // one record buffer
   static constexpr int CSTRIDE = N * N + 2;              // staging stride: (stride/2) odd
   static constexpr int STG_DBL = CELLS * CSTRIDE;
-  static constexpr int UNION = REC_DBL > STG_DBL ? REC_DBL : STG_DBL;
   static constexpr int TAB0 = Q + 3 * Q * NS + 4 * Q;    // W | D | P
   static constexpr int TAB = (TAB0 + 1) / 2 * 2;
-  static constexpr int CELLD = 12 + 10;                  // coords | K(9), adet
-  static constexpr int IN_DBL = CELLS * (12 + NCOEF);    // raw inputs (cp.async target)
+  static constexpr int CELLD = 10;                       // K(9), adet
+  static constexpr int IN_DBL = CELLS * (12 + NCOEF);    // raw inputs
   static constexpr int QD_DBL = SVK ? QC * CELLS * QDD : 0;
-  static constexpr size_t SMEM =
-      sizeof(double) * ((size_t)TAB + CELLS * CELLD + IN_DBL + QD_DBL + UNION);
+  static constexpr int HEAD = TAB + CELLS * CELLD + IN_DBL + QD_DBL;
+  // ws: two record buffers + separate staging; flat: one record buffer aliasing staging
+  static constexpr int BODY = SVK ? (REC_DBL > STG_DBL ? REC_DBL : STG_DBL)
+                                  : 2 * REC_DBL + STG_DBL;
+  static constexpr size_t SMEM = sizeof(double) * ((size_t)HEAD + BODY) + 4 * sizeof(uint64_t);
   static_assert(NS % 2 == 0, "2x2 tiling needs an even number of scalar dofs");
-  static_assert(CELLS * (NTILE + 1) <= THREADS, "one (cell, tile) per thread");
+  static_assert(CELLS * (NTILE + 1) <= ACC, "one (cell, tile) per accumulating thread");
   static_assert((CSTRIDE / 2) % 2 == 1, "conflict-free staging stride");
+  static_assert(HEAD % 2 == 0 && REC_DBL % 2 == 0, "16-byte aligned buffers");
 };
 
+__device__ __forceinline__ void mbar_arrive_cta(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 
-template <int KIND, int NS, int Q>
-__global__ void __launch_bounds__(128, PairShape<KIND, NS, Q>::CTAS_PER_SM)
-    pair_kernel(long E, const double* __restrict__ coords, const double* __restrict__ coef,
-                const double* __restrict__ tab, double* __restrict__ A, int acc) {
-  using Sh = PairShape<KIND, NS, Q>;
-  constexpr int N = Sh::N, CELLS = Sh::CELLS;
+// (cell, tile) of an accumulating thread: tile t -> upper 2x2 block (TJ, TK)
+struct PairSlot {
+  int cell, j0, k0;
+  bool active, diag;
+};
+template <class Sh>
+__device__ __forceinline__ PairSlot pair_slot(int tid) {
+  PairSlot s;
+  s.cell = tid % Sh::CELLS;
+  const int my_tile = tid / Sh::CELLS;
+  s.active = my_tile < Sh::NTILE;
+  int TJ = 0, TK = 0, t = s.active ? my_tile : 0;
+  for (int J = 0; J < Sh::NJ; ++J) {
+    const int len = Sh::NJ - J;
+    if (t < len) {
+      TJ = J;
+      TK = J + t;
+      break;
+    }
+    t -= len;
+  }
+  s.j0 = 2 * TJ;
+  s.k0 = 2 * TK;
+  s.diag = TJ == TK;
+  return s;
+}
+
+// Accumulate one quadrature point's records into the thread's 2x2 tile.
+template <class Sh>
+__device__ __forceinline__ void pair_point(double (&a4)[2][2][3][3], const double* rq,
+                                           const double* qs, int j0, int k0) {
+  constexpr int CELLS = Sh::CELLS, JS = Sh::JS;
+  const double lq = qs[0], mq = qs[CELLS];
+  double gk[2][3];
+#pragma unroll
+  for (int y = 0; y < 2; ++y)
+#pragma unroll
+    for (int bb = 0; bb < 3; ++bb) gk[y][bb] = rq[(k0 + y) * JS + bb * CELLS];
+  if constexpr (!Sh::SVK) {
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+      double u[3], v[3];
+#pragma unroll
+      for (int bb = 0; bb < 3; ++bb) {
+        const double gj = rq[(j0 + x) * JS + bb * CELLS];
+        u[bb] = mq * gj;
+        v[bb] = lq * gj;
+      }
+      // independent FMA passes (no dependent pairs back to back)
+#pragma unroll
+      for (int y = 0; y < 2; ++y)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int d = 0; d < 3; ++d) a4[x][y][c][d] = fma(v[c], gk[y][d], a4[x][y][c][d]);
+#pragma unroll
+      for (int y = 0; y < 2; ++y)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int d = 0; d < 3; ++d) a4[x][y][c][d] = fma(u[d], gk[y][c], a4[x][y][c][d]);
+#pragma unroll
+      for (int y = 0; y < 2; ++y) {
+        const double S = u[0] * gk[y][0] + u[1] * gk[y][1] + u[2] * gk[y][2];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) a4[x][y][c][c] += S;
+      }
+    }
+  } else {
+    double hk[2][3];
+#pragma unroll
+    for (int y = 0; y < 2; ++y)
+#pragma unroll
+      for (int bb = 0; bb < 3; ++bb) hk[y][bb] = rq[(k0 + y) * JS + (3 + bb) * CELLS];
+    const double f00 = qs[2 * CELLS], f01 = qs[3 * CELLS], f02 = qs[4 * CELLS];
+    const double f11 = qs[5 * CELLS], f12 = qs[6 * CELLS], f22 = qs[7 * CELLS];
+    const double ff[3][3] = {{f00, f01, f02}, {f01, f11, f12}, {f02, f12, f22}};
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+      double gj[3], lh[3], mh[3], s[3];
+      const double* r = rq + (j0 + x) * JS;
+#pragma unroll
+      for (int bb = 0; bb < 3; ++bb) {
+        gj[bb] = mq * r[bb * CELLS];           // mu' g_j
+        const double h = r[(3 + bb) * CELLS];
+        lh[bb] = lq * h;                       // lam' h_j
+        mh[bb] = mq * h;                       // mu' h_j
+        s[bb] = r[(6 + bb) * CELLS];           // w' S g_j
+      }
+      double t1[2], t2[2];
+#pragma unroll
+      for (int y = 0; y < 2; ++y) {
+        t1[y] = s[0] * gk[y][0] + s[1] * gk[y][1] + s[2] * gk[y][2];
+        t2[y] = gj[0] * gk[y][0] + gj[1] * gk[y][1] + gj[2] * gk[y][2];
+      }
+#pragma unroll
+      for (int y = 0; y < 2; ++y)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int d = 0; d < 3; ++d) a4[x][y][c][d] = fma(lh[c], hk[y][d], a4[x][y][c][d]);
+#pragma unroll
+      for (int y = 0; y < 2; ++y)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int d = 0; d < 3; ++d) a4[x][y][c][d] = fma(hk[y][c], mh[d], a4[x][y][c][d]);
+#pragma unroll
+      for (int y = 0; y < 2; ++y)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int d = 0; d < 3; ++d) a4[x][y][c][d] = fma(t2[y], ff[c][d], a4[x][y][c][d]);
+#pragma unroll
+      for (int y = 0; y < 2; ++y)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) a4[x][y][c][c] += t1[y];
+    }
+  }
+}
+
+// The tile's symmetric half, mirrored, into the cell's staging row.
+template <class Sh>
+__device__ __forceinline__ void pair_stage(double* stg, const double (&a4)[2][2][3][3],
+                                           const PairSlot& sl) {
+  constexpr int N = Sh::N, NS = N / 3;
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int d = 0; d < 3; ++d)
+        // row (c, j0+x), columns (d, k0..k0+1): one 16-byte store
+        *reinterpret_cast<double2*>(&stg[(c * NS + sl.j0 + x) * N + d * NS + sl.k0]) =
+            make_double2(a4[x][0][c][d], a4[x][1][c][d]);
+  if (!sl.diag) {
+#pragma unroll
+    for (int y = 0; y < 2; ++y)
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+          // mirror: row (d, k0+y), columns (c, j0..j0+1)
+          *reinterpret_cast<double2*>(&stg[(d * NS + sl.k0 + y) * N + c * NS + sl.j0]) =
+              make_double2(a4[0][y][c][d], a4[1][y][c][d]);
+  } else {
+    // diagonal tile: entry (j0+1, k0) is the mirror of (j0, k0+1)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int d = 0; d < 3; ++d) stg[(d * NS + sl.k0 + 1) * N + c * NS + sl.j0] = a4[0][1][c][d];
+  }
+}
+
+// Staged element matrices -> global by the TMA engine (one thread issues).
+template <class Sh>
+__device__ __forceinline__ void pair_bulk_store(double* A, long c0, int nt, const double* stg,
+                                                int acc) {
+  constexpr int N = Sh::N;
+  for (int c = 0; c < nt; ++c) {
+    double* dst = A + (c0 + c) * (size_t)N * N;
+    if (acc)
+      bulk_s2g_add(dst, stg + c * Sh::CSTRIDE, N * N * 8);
+    else
+      bulk_s2g(dst, stg + c * Sh::CSTRIDE, N * N * 8);
+  }
+  bulk_commit();
+}
+
+__device__ __forceinline__ void zero_tile(double (&a4)[2][2][3][3]) {
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int y = 0; y < 2; ++y)
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) a4[x][y][c][d] = 0.0;
+}
+
+// ============================================================================
+// Elasticity: warp-specialised (2 producer warps, 4 consumer warps)
+// ============================================================================
+template <int NS, int Q>
+__global__ void __launch_bounds__(PairShape<FEMGPU_ELASTICITY, NS, Q>::THREADS, 2)
+    pair_ws_kernel(long E, const double* __restrict__ coords, const double* __restrict__ coef,
+                   const double* __restrict__ tab, double* __restrict__ A, int acc) {
+  using Sh = PairShape<FEMGPU_ELASTICITY, NS, Q>;
+  constexpr int CELLS = Sh::CELLS;
+  extern __shared__ __align__(16) double smem[];
+  double* sW = smem;
+  double* sD = sW + Q;                      // [3][Q][NS]
+  double* sP = sD + 3 * Q * NS;             // [Q][4]
+  double* sCell = smem + Sh::TAB;           // [CELLS][CELLD]    (producer)
+  double* sIn = sCell + CELLS * Sh::CELLD;  // [CELLS][12] | [CELLS][NCOEF]  (producer)
+  double* sRec = sIn + Sh::IN_DBL;          // [2][REC_DBL]  producer -> consumers
+  double* sStg = sRec + 2 * Sh::REC_DBL;    // [CELLS][CSTRIDE]  consumers -> TMA
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStg + Sh::STG_DBL);
+  uint64_t* empty = full + 2;
+  // record buffer: rec[(q*NS + j)*JS + comp*CELLS + cell], then qs[(q*QSD + x)*CELLS + cell]
+
+  const int tid = threadIdx.x;
+  const long ntiles = (E + CELLS - 1) / CELLS;
+  if ((long)blockIdx.x >= ntiles) return;
+  const long my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+
+  for (int i = tid; i < Sh::TAB0; i += Sh::THREADS) smem[i] = tab[i];
+  if (tid == 0) {
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&full[b], Sh::PROD);
+      mbar_init(&empty[b], Sh::ACC / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (tid < Sh::ACC) {
+    // ---------------- consumers ----------------
+    const PairSlot sl = pair_slot<Sh>(tid);
+    const int lane = tid & 31;
+    for (long it = 0; it < my_tiles; ++it) {
+      const long c0 = (blockIdx.x + it * gridDim.x) * CELLS;
+      const int nt = (int)min((long)CELLS, E - c0);
+      const int b = (int)(it & 1);
+      double a4[2][2][3][3];
+      zero_tile(a4);
+      mbar_wait(&full[b], (uint32_t)((it >> 1) & 1));
+      const double* rec = sRec + b * Sh::REC_DBL;
+      const double* qsb = rec + Q * NS * Sh::JS;
+      if (sl.active) {
+#pragma unroll 1
+        for (int q = 0; q < Q; ++q)
+          pair_point<Sh>(a4, rec + q * NS * Sh::JS + sl.cell, qsb + q * Sh::QSD * CELLS + sl.cell,
+                         sl.j0, sl.k0);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cta(&empty[b]);
+      if (tid == 0) bulk_wait_read0();  // previous tile's bulk stores have read the staging
+      named_bar(1, Sh::ACC);
+      if (sl.active) pair_stage<Sh>(sStg + sl.cell * Sh::CSTRIDE, a4, sl);
+      fence_proxy_async();
+      named_bar(1, Sh::ACC);
+      if (tid == 0) pair_bulk_store<Sh>(A, c0, nt, sStg, acc);
+    }
+    if (tid == 0) bulk_wait0();
+  } else {
+    // ---------------- producers: inputs, geometry, records of tile it ----------------
+    const int pt = tid - Sh::ACC;
+    for (long it = 0; it < my_tiles; ++it) {
+      const long c0 = (blockIdx.x + it * gridDim.x) * CELLS;
+      const int nt = (int)min((long)CELLS, E - c0);
+      const int b = (int)(it & 1);
+      for (int i = pt; i < CELLS * 12; i += Sh::PROD) {
+        const int c = i / 12, r = i % 12;  // cells past the end: reference tet
+        sIn[i] = c < nt ? coords[(c0 + c) * 12 + r] : ((r == 3 || r == 7 || r == 11) ? 1.0 : 0.0);
+      }
+      for (int i = pt; i < CELLS * Sh::NCOEF; i += Sh::PROD)
+        sIn[CELLS * 12 + i] = (i / Sh::NCOEF) < nt ? coef[c0 * Sh::NCOEF + i] : 0.0;
+      named_bar(2, Sh::PROD);
+      if (pt < CELLS) {
+        const Geo g = cell_geometry(&sIn[pt * 12]);
+        double* cd = sCell + pt * Sh::CELLD;
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int bb = 0; bb < 3; ++bb) cd[a * 3 + bb] = g.K[a][bb];
+        cd[9] = g.adet;
+      }
+      named_bar(2, Sh::PROD);
+      if (it >= 2) mbar_wait(&empty[b], (uint32_t)(((it >> 1) - 1) & 1));
+      double* rec = sRec + b * Sh::REC_DBL;
+      double* qsb = rec + Q * NS * Sh::JS;
+      for (int task = pt; task < CELLS * Q * NS; task += Sh::PROD) {
+        const int c = task % CELLS, r = task / CELLS;
+        const int j = r % NS, q = r / NS;
+        const double* K = sCell + c * Sh::CELLD;
+        double* rr = rec + (q * NS + j) * Sh::JS + c;
+#pragma unroll
+        for (int bb = 0; bb < 3; ++bb)
+          rr[bb * CELLS] = K[0 * 3 + bb] * sD[(0 * Q + q) * NS + j] +
+                           K[1 * 3 + bb] * sD[(1 * Q + q) * NS + j] +
+                           K[2 * 3 + bb] * sD[(2 * Q + q) * NS + j];
+        if (j == 0) {
+          const double* cf = sIn + CELLS * 12 + c * Sh::NCOEF;
+          double muq = 0, lamq = 0;
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            muq += cf[m] * sP[q * 4 + m];
+            lamq += cf[4 + m] * sP[q * 4 + m];
+          }
+          const double wq = sW[q] * K[9];
+          double* qs = qsb + q * Sh::QSD * CELLS + c;
+          qs[0] = lamq * wq;
+          qs[CELLS] = muq * wq;
+        }
+      }
+      mbar_arrive_cta(&full[b]);  // release: this tile's records are visible
+      named_bar(2, Sh::PROD);     // sIn / sCell reused by the next tile
+    }
+  }
+}
+
+// ============================================================================
+// St Venant-Kirchhoff: flat (all threads in every phase), 2 CTAs per SM
+// ============================================================================
+template <int NS, int Q>
+__global__ void __launch_bounds__(128, 2)
+    pair_flat_kernel(long E, const double* __restrict__ coords, const double* __restrict__ coef,
+                     const double* __restrict__ tab, double* __restrict__ A, int acc) {
+  using Sh = PairShape<FEMGPU_HYPERELASTICITY, NS, Q>;
+  constexpr int CELLS = Sh::CELLS;
   extern __shared__ __align__(16) double smem[];
   double* sW = smem;
   double* sD = sW + Q;                      // [3][Q][NS]
   double* sP = sD + 3 * Q * NS;             // [Q][4]
   double* sCell = smem + Sh::TAB;           // [CELLS][CELLD]
   double* sIn = sCell + CELLS * Sh::CELLD;  // [CELLS][12] | [CELLS][NCOEF]
-  double* sQd = sIn + Sh::IN_DBL;           // SVK: [QC][CELLS][QDD]
-  double* sU = sQd + Sh::QD_DBL;            // records (chunk) / output staging
-  // record layout: rec[((ql*NS + j)*RECD + comp)*CELLS + cell], then per-q scalars
-  double* sQs = sU + Sh::QC * NS * Sh::RECD * CELLS;  // [QC][QSD][CELLS]
+  double* sQd = sIn + Sh::IN_DBL;           // [QC][CELLS][QDD]
+  double* sU = sQd + Sh::QD_DBL;            // records of a chunk / output staging
+  double* sQs = sU + Sh::QC * NS * Sh::JS;  // [QC][QSD][CELLS]
 
   const int tid = threadIdx.x;
   for (int i = tid; i < Sh::TAB0; i += Sh::THREADS) smem[i] = tab[i];
-
-  const int cell = tid % CELLS;
-  const int my_tile = tid / CELLS;
-  const bool active = my_tile < Sh::NTILE;
-  int TJ = 0, TK = 0;
-  {
-    int t = active ? my_tile : 0;
-    for (int J = 0; J < Sh::NJ; ++J) {
-      const int len = Sh::NJ - J;
-      if (t < len) {
-        TJ = J;
-        TK = J + t;
-        break;
-      }
-      t -= len;
-    }
-  }
-  const int j0 = 2 * TJ, k0 = 2 * TK;
+  const PairSlot sl = pair_slot<Sh>(tid);
 
   const long ntiles = (E + CELLS - 1) / CELLS;
   auto prefetch = [&](long tile) {
@@ -136,271 +444,109 @@ __global__ void __launch_bounds__(128, PairShape<KIND, NS, Q>::CTAS_PER_SM)
 #pragma unroll
       for (int a = 0; a < 3; ++a)
 #pragma unroll
-        for (int b = 0; b < 3; ++b) cd[12 + a * 3 + b] = g.K[a][b];
-      cd[21] = g.adet;
+        for (int b = 0; b < 3; ++b) cd[a * 3 + b] = g.K[a][b];
+      cd[9] = g.adet;
     }
     __syncthreads();
     auto coefv = [&](int c, int r) -> double {
       return c < nt ? sIn[CELLS * 12 + c * Sh::NCOEF + r] : 0.0;
     };
-
     double a4[2][2][3][3];
-#pragma unroll
-    for (int x = 0; x < 2; ++x)
-#pragma unroll
-      for (int y = 0; y < 2; ++y)
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-#pragma unroll
-          for (int d = 0; d < 3; ++d) a4[x][y][c][d] = 0.0;
-
+    zero_tile(a4);
 #pragma unroll 1
     for (int ch = 0; ch < Sh::NCHUNK; ++ch) {
       const int q0 = ch * Sh::QC;
       const int qn = min(Sh::QC, Q - q0);
-      if constexpr (Sh::SVK) {
-        // ---- per (cell, q): F = I + grad w, w' S, F F^T, lam', mu' ---------
-        for (int task = tid; task < CELLS * qn; task += Sh::THREADS) {
-          const int c = task % CELLS, ql = task / CELLS, q = q0 + ql;
-          const double* cd = sCell + c * Sh::CELLD;
-          const double* K = cd + 12;
-          double muq = 0, lamq = 0;
+      // ---- per (cell, q): F = I + grad w, w' S, F F^T, lam', mu' ------------
+      for (int task = tid; task < CELLS * qn; task += Sh::THREADS) {
+        const int c = task % CELLS, ql = task / CELLS, q = q0 + ql;
+        const double* K = sCell + c * Sh::CELLD;
+        double muq = 0, lamq = 0;
 #pragma unroll
-          for (int m = 0; m < 4; ++m) {
-            muq += coefv(c, 3 * NS + m) * sP[q * 4 + m];
-            lamq += coefv(c, 3 * NS + 4 + m) * sP[q * 4 + m];
-          }
-          const double wq = sW[q] * cd[21];
-          double F[3][3];
-#pragma unroll
-          for (int cc = 0; cc < 3; ++cc) {
-            double gr[3] = {0, 0, 0};  // reference gradient of w_cc
-#pragma unroll
-            for (int m = 0; m < NS; ++m) {
-              const double wm = coefv(c, cc * NS + m);
-#pragma unroll
-              for (int a = 0; a < 3; ++a) gr[a] += wm * sD[(a * Q + q) * NS + m];
-            }
-#pragma unroll
-            for (int b = 0; b < 3; ++b)
-              F[cc][b] = (cc == b ? 1.0 : 0.0) + gr[0] * K[0 * 3 + b] + gr[1] * K[1 * 3 + b] +
-                         gr[2] * K[2 * 3 + b];
-          }
-          double Ee[3][3];
-#pragma unroll
-          for (int a = 0; a < 3; ++a)
-#pragma unroll
-            for (int b = 0; b < 3; ++b) {
-              const double t = F[0][a] * F[0][b] + F[1][a] * F[1][b] + F[2][a] * F[2][b];
-              Ee[a][b] = 0.5 * (a == b ? t - 1.0 : t);
-            }
-          const double trE = Ee[0][0] + Ee[1][1] + Ee[2][2];
-          double* qd = sQd + (ql * CELLS + c) * Sh::QDD;
-#pragma unroll
-          for (int a = 0; a < 3; ++a)
-#pragma unroll
-            for (int b = 0; b < 3; ++b) {
-              qd[a * 3 + b] = F[a][b];
-              qd[9 + a * 3 + b] = wq * ((a == b ? lamq * trE : 0.0) + 2.0 * muq * Ee[a][b]);
-            }
-          double* qs = sQs + ql * Sh::QSD * CELLS + c;
-          qs[0 * CELLS] = lamq * wq;
-          qs[1 * CELLS] = muq * wq;
-          // F F^T: (0,0),(0,1),(0,2),(1,1),(1,2),(2,2)
-          qs[2 * CELLS] = F[0][0] * F[0][0] + F[0][1] * F[0][1] + F[0][2] * F[0][2];
-          qs[3 * CELLS] = F[0][0] * F[1][0] + F[0][1] * F[1][1] + F[0][2] * F[1][2];
-          qs[4 * CELLS] = F[0][0] * F[2][0] + F[0][1] * F[2][1] + F[0][2] * F[2][2];
-          qs[5 * CELLS] = F[1][0] * F[1][0] + F[1][1] * F[1][1] + F[1][2] * F[1][2];
-          qs[6 * CELLS] = F[1][0] * F[2][0] + F[1][1] * F[2][1] + F[1][2] * F[2][2];
-          qs[7 * CELLS] = F[2][0] * F[2][0] + F[2][1] * F[2][1] + F[2][2] * F[2][2];
+        for (int m = 0; m < 4; ++m) {
+          muq += coefv(c, 3 * NS + m) * sP[q * 4 + m];
+          lamq += coefv(c, 3 * NS + 4 + m) * sP[q * 4 + m];
         }
-        __syncthreads();
+        const double wq = sW[q] * K[9];
+        double F[3][3];
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) {
+          double gr[3] = {0, 0, 0};  // reference gradient of w_cc
+#pragma unroll
+          for (int m = 0; m < NS; ++m) {
+            const double wm = coefv(c, cc * NS + m);
+#pragma unroll
+            for (int a = 0; a < 3; ++a) gr[a] += wm * sD[(a * Q + q) * NS + m];
+          }
+#pragma unroll
+          for (int b = 0; b < 3; ++b)
+            F[cc][b] = (cc == b ? 1.0 : 0.0) + gr[0] * K[0 * 3 + b] + gr[1] * K[1 * 3 + b] +
+                       gr[2] * K[2 * 3 + b];
+        }
+        double Ee[3][3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int b = 0; b < 3; ++b) {
+            const double t = F[0][a] * F[0][b] + F[1][a] * F[1][b] + F[2][a] * F[2][b];
+            Ee[a][b] = 0.5 * (a == b ? t - 1.0 : t);
+          }
+        const double trE = Ee[0][0] + Ee[1][1] + Ee[2][2];
+        double* qd = sQd + (ql * CELLS + c) * Sh::QDD;
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int b = 0; b < 3; ++b) {
+            qd[a * 3 + b] = F[a][b];
+            qd[9 + a * 3 + b] = wq * ((a == b ? lamq * trE : 0.0) + 2.0 * muq * Ee[a][b]);
+          }
+        double* qs = sQs + ql * Sh::QSD * CELLS + c;
+        qs[0 * CELLS] = lamq * wq;
+        qs[1 * CELLS] = muq * wq;
+        // F F^T: (0,0),(0,1),(0,2),(1,1),(1,2),(2,2)
+        qs[2 * CELLS] = F[0][0] * F[0][0] + F[0][1] * F[0][1] + F[0][2] * F[0][2];
+        qs[3 * CELLS] = F[0][0] * F[1][0] + F[0][1] * F[1][1] + F[0][2] * F[1][2];
+        qs[4 * CELLS] = F[0][0] * F[2][0] + F[0][1] * F[2][1] + F[0][2] * F[2][2];
+        qs[5 * CELLS] = F[1][0] * F[1][0] + F[1][1] * F[1][1] + F[1][2] * F[1][2];
+        qs[6 * CELLS] = F[1][0] * F[2][0] + F[1][1] * F[2][1] + F[1][2] * F[2][2];
+        qs[7 * CELLS] = F[2][0] * F[2][0] + F[2][1] * F[2][1] + F[2][2] * F[2][2];
       }
-      // ---- records of the chunk: per (cell, q, j) -------------------------
+      __syncthreads();
+      // ---- records of the chunk: per (cell, q, j): g, h = F g, s = w' S g ----
       for (int task = tid; task < CELLS * qn * NS; task += Sh::THREADS) {
         const int c = task % CELLS, r = task / CELLS;
         const int j = r % NS, ql = r / NS, q = q0 + ql;
-        const double* cd = sCell + c * Sh::CELLD;
-        const double* K = cd + 12;
+        const double* K = sCell + c * Sh::CELLD;
         double g[3];
 #pragma unroll
         for (int b = 0; b < 3; ++b)
           g[b] = K[0 * 3 + b] * sD[(0 * Q + q) * NS + j] + K[1 * 3 + b] * sD[(1 * Q + q) * NS + j] +
                  K[2 * 3 + b] * sD[(2 * Q + q) * NS + j];
-        double* rec = sU + ((ql * NS + j) * Sh::RECD) * CELLS + c;
+        double* rr = sU + (ql * NS + j) * Sh::JS + c;
+        const double* qd = sQd + (ql * CELLS + c) * Sh::QDD;
 #pragma unroll
-        for (int b = 0; b < 3; ++b) rec[b * CELLS] = g[b];
-        if constexpr (Sh::SVK) {
-          const double* qd = sQd + (ql * CELLS + c) * Sh::QDD;
+        for (int b = 0; b < 3; ++b) rr[b * CELLS] = g[b];
 #pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            rec[(3 + a) * CELLS] = qd[a * 3 + 0] * g[0] + qd[a * 3 + 1] * g[1] + qd[a * 3 + 2] * g[2];
-            rec[(6 + a) * CELLS] =
-                qd[9 + a * 3 + 0] * g[0] + qd[9 + a * 3 + 1] * g[1] + qd[9 + a * 3 + 2] * g[2];
-          }
-        } else if (j == 0) {
-          double muq = 0, lamq = 0;
-#pragma unroll
-          for (int m = 0; m < 4; ++m) {
-            muq += coefv(c, m) * sP[q * 4 + m];
-            lamq += coefv(c, 4 + m) * sP[q * 4 + m];
-          }
-          const double wq = sW[q] * cd[21];
-          double* qs = sQs + ql * Sh::QSD * CELLS + c;
-          qs[0] = lamq * wq;
-          qs[CELLS] = muq * wq;
+        for (int a = 0; a < 3; ++a) {
+          rr[(3 + a) * CELLS] = qd[a * 3 + 0] * g[0] + qd[a * 3 + 1] * g[1] + qd[a * 3 + 2] * g[2];
+          rr[(6 + a) * CELLS] =
+              qd[9 + a * 3 + 0] * g[0] + qd[9 + a * 3 + 1] * g[1] + qd[9 + a * 3 + 2] * g[2];
         }
       }
       __syncthreads();
       if (ch == Sh::NCHUNK - 1 && tile + gridDim.x < ntiles) prefetch(tile + gridDim.x);
-      // ---- accumulate (no synchronisation inside) --------------------------
-      if (active) {
+      if (sl.active) {
 #pragma unroll 1
-        for (int ql = 0; ql < qn; ++ql) {
-          const double* rq = sU + ql * NS * Sh::RECD * CELLS + cell;
-          const double* qs = sQs + ql * Sh::QSD * CELLS + cell;
-          const double lq = qs[0], mq = qs[CELLS];
-          double gk[2][3];
-#pragma unroll
-          for (int y = 0; y < 2; ++y)
-#pragma unroll
-            for (int b = 0; b < 3; ++b) gk[y][b] = rq[((k0 + y) * Sh::RECD + b) * CELLS];
-          if constexpr (!Sh::SVK) {
-#pragma unroll
-            for (int x = 0; x < 2; ++x) {
-              double u[3], v[3];
-#pragma unroll
-              for (int b = 0; b < 3; ++b) {
-                const double gj = rq[((j0 + x) * Sh::RECD + b) * CELLS];
-                u[b] = mq * gj;
-                v[b] = lq * gj;
-              }
-              // independent FMA passes (no dependent pairs back to back)
-#pragma unroll
-              for (int y = 0; y < 2; ++y)
-#pragma unroll
-                for (int c = 0; c < 3; ++c)
-#pragma unroll
-                  for (int d = 0; d < 3; ++d) a4[x][y][c][d] = fma(v[c], gk[y][d], a4[x][y][c][d]);
-#pragma unroll
-              for (int y = 0; y < 2; ++y)
-#pragma unroll
-                for (int c = 0; c < 3; ++c)
-#pragma unroll
-                  for (int d = 0; d < 3; ++d) a4[x][y][c][d] = fma(u[d], gk[y][c], a4[x][y][c][d]);
-#pragma unroll
-              for (int y = 0; y < 2; ++y) {
-                const double S = u[0] * gk[y][0] + u[1] * gk[y][1] + u[2] * gk[y][2];
-#pragma unroll
-                for (int c = 0; c < 3; ++c) a4[x][y][c][c] += S;
-              }
-            }
-          } else {
-            double hk[2][3];
-#pragma unroll
-            for (int y = 0; y < 2; ++y)
-#pragma unroll
-              for (int b = 0; b < 3; ++b) hk[y][b] = rq[((k0 + y) * Sh::RECD + 3 + b) * CELLS];
-            const double f00 = qs[2 * CELLS], f01 = qs[3 * CELLS], f02 = qs[4 * CELLS];
-            const double f11 = qs[5 * CELLS], f12 = qs[6 * CELLS], f22 = qs[7 * CELLS];
-            const double ff[3][3] = {{f00, f01, f02}, {f01, f11, f12}, {f02, f12, f22}};
-#pragma unroll
-            for (int x = 0; x < 2; ++x) {
-              double gj[3], lh[3], mh[3], s[3];
-#pragma unroll
-              for (int b = 0; b < 3; ++b) {
-                const double* r = rq + ((j0 + x) * Sh::RECD) * CELLS;
-                gj[b] = mq * r[b * CELLS];           // mu' g_j
-                const double h = r[(3 + b) * CELLS];
-                lh[b] = lq * h;                      // lam' h_j
-                mh[b] = mq * h;                      // mu' h_j
-                s[b] = r[(6 + b) * CELLS];           // w' S g_j
-              }
-              double t1[2], t2[2];
-#pragma unroll
-              for (int y = 0; y < 2; ++y) {
-                t1[y] = s[0] * gk[y][0] + s[1] * gk[y][1] + s[2] * gk[y][2];
-                t2[y] = gj[0] * gk[y][0] + gj[1] * gk[y][1] + gj[2] * gk[y][2];
-              }
-              // independent FMA passes over the 18 accumulators of this j
-#pragma unroll
-              for (int y = 0; y < 2; ++y)
-#pragma unroll
-                for (int c = 0; c < 3; ++c)
-#pragma unroll
-                  for (int d = 0; d < 3; ++d) a4[x][y][c][d] = fma(lh[c], hk[y][d], a4[x][y][c][d]);
-#pragma unroll
-              for (int y = 0; y < 2; ++y)
-#pragma unroll
-                for (int c = 0; c < 3; ++c)
-#pragma unroll
-                  for (int d = 0; d < 3; ++d) a4[x][y][c][d] = fma(hk[y][c], mh[d], a4[x][y][c][d]);
-#pragma unroll
-              for (int y = 0; y < 2; ++y)
-#pragma unroll
-                for (int c = 0; c < 3; ++c)
-#pragma unroll
-                  for (int d = 0; d < 3; ++d) a4[x][y][c][d] = fma(t2[y], ff[c][d], a4[x][y][c][d]);
-#pragma unroll
-              for (int y = 0; y < 2; ++y)
-#pragma unroll
-                for (int c = 0; c < 3; ++c) a4[x][y][c][c] += t1[y];
-            }
-          }
-        }
+        for (int ql = 0; ql < qn; ++ql)
+          pair_point<Sh>(a4, sU + ql * NS * Sh::JS + sl.cell, sQs + ql * Sh::QSD * CELLS + sl.cell,
+                         sl.j0, sl.k0);
       }
       __syncthreads();  // records consumed (next chunk / staging overwrite them)
     }
-
-    // ---- epilogue: mirror into staging (all 16 cells), coalesced stores -----
-    double* stg = sU + cell * Sh::CSTRIDE;
-    if (active) {
-#pragma unroll
-      for (int x = 0; x < 2; ++x)
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-#pragma unroll
-          for (int d = 0; d < 3; ++d) {
-            const int j = j0 + x;
-            // row (c, j), columns (d, k0..k0+1): one 16-byte store
-            *reinterpret_cast<double2*>(&stg[(c * NS + j) * N + d * NS + k0]) =
-                make_double2(a4[x][0][c][d], a4[x][1][c][d]);
-          }
-      if (TJ != TK) {
-#pragma unroll
-        for (int y = 0; y < 2; ++y)
-#pragma unroll
-          for (int c = 0; c < 3; ++c)
-#pragma unroll
-            for (int d = 0; d < 3; ++d) {
-              const int k = k0 + y;
-              // mirror: row (d, k), columns (c, j0..j0+1)
-              *reinterpret_cast<double2*>(&stg[(d * NS + k) * N + c * NS + j0]) =
-                  make_double2(a4[0][y][c][d], a4[1][y][c][d]);
-            }
-      } else {
-        // diagonal tile: entry (j0+1, k0) is the mirror of (j0, k0+1)
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-#pragma unroll
-          for (int d = 0; d < 3; ++d)
-            stg[(d * NS + k0 + 1) * N + c * NS + j0] = a4[0][1][c][d];
-      }
-    }
-    // staged element matrices -> global by the TMA engine (async bulk copies,
-    // or bulk reductions for the += contract); threads move on immediately
+    if (sl.active) pair_stage<Sh>(sU + sl.cell * Sh::CSTRIDE, a4, sl);
     fence_proxy_async();
     __syncthreads();
-    if (tid == 0) {
-      for (int c = 0; c < nt; ++c) {
-        double* dst = A + (c0 + c) * (size_t)N * N;
-        if (acc)
-          bulk_s2g_add(dst, sU + c * Sh::CSTRIDE, N * N * 8);
-        else
-          bulk_s2g(dst, sU + c * Sh::CSTRIDE, N * N * 8);
-      }
-      bulk_commit();
-    }
+    if (tid == 0) pair_bulk_store<Sh>(A, c0, nt, sU, acc);
   }
   if (tid == 0) bulk_wait0();
 }
@@ -409,17 +555,18 @@ template <int KIND, int NS, int Q>
 static cudaError_t launch_pair_t(long E, const double* coords, const double* coef,
                                  const double* tab, double* A, int acc, cudaStream_t s) {
   using Sh = PairShape<KIND, NS, Q>;
+  auto kern = Sh::SVK ? pair_flat_kernel<NS, Q> : pair_ws_kernel<NS, Q>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(pair_kernel<KIND, NS, Q>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::SMEM);
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::SMEM);
     if (e != cudaSuccess) return e;
     configured = true;
   }
   const long ntiles = (E + Sh::CELLS - 1) / Sh::CELLS;
   const long maxc = (long)Sh::CTAS_PER_SM * kNumSMs;
   const int grid = (int)(ntiles < maxc ? ntiles : maxc);
-  pair_kernel<KIND, NS, Q><<<grid, Sh::THREADS, Sh::SMEM, s>>>(E, coords, coef, tab, A, acc);
+  kern<<<grid, Sh::THREADS, Sh::SMEM, s>>>(E, coords, coef, tab, A, acc);
   return cudaGetLastError();
 }
 
