@@ -41,6 +41,10 @@
 #include "femgpu_internal.h"
 #include "../../include/femgpu.h"
 
+#ifndef PAIR_ELAS_FLAT
+#define PAIR_ELAS_FLAT 0
+#endif
+
 namespace femgpu {
 
 template <int KIND, int NS, int Q>
@@ -51,7 +55,8 @@ struct PairShape {
   static constexpr int NTILE = NJ * (NJ + 1) / 2;        // 2x2 tiles on/above the diagonal
   static constexpr int CELLS = 8;                        // cells per CTA tile
   static constexpr int ACC = 128;                        // accumulating threads: 8 x 16 slots
-  static constexpr int PROD = SVK ? 0 : 64;              // producer threads (ws kernel only)
+  static constexpr bool FLAT = SVK || PAIR_ELAS_FLAT;    // organisation (see header)
+  static constexpr int PROD = FLAT ? 0 : 64;             // producer threads (ws kernel only)
   static constexpr int THREADS = ACC + PROD;
   static constexpr int CTAS_PER_SM = 2;
   static constexpr int NCOEF = SVK ? 3 * NS + 8 : 8;
@@ -59,7 +64,6 @@ struct PairShape {
   static constexpr int NCHUNK = (Q + QC - 1) / QC;
   static constexpr int RECD = SVK ? 9 : 3;               // per (q,j): g | h | s
   static constexpr int QSD = SVK ? 8 : 2;                // per q: lam', mu' | F F^T (6)
-  static constexpr int QDD = 18;                         // SVK per (cell,q): F, w'S
   // j-stride of a record buffer: RECD*CELLS + 4 doubles, so the k-side loads of the
   // (j,k) tiles sharing a warp (k0 two apart) fall in alternate bank halves
   static constexpr int JS = RECD * CELLS + 4;
@@ -70,11 +74,10 @@ struct PairShape {
   static constexpr int TAB = (TAB0 + 1) / 2 * 2;
   static constexpr int CELLD = 10;                       // K(9), adet
   static constexpr int IN_DBL = CELLS * (12 + NCOEF);    // raw inputs
-  static constexpr int QD_DBL = SVK ? QC * CELLS * QDD : 0;
-  static constexpr int HEAD = TAB + CELLS * CELLD + IN_DBL + QD_DBL;
+  static constexpr int HEAD = TAB + CELLS * CELLD + (FLAT ? 1 : 2) * IN_DBL;  // ws: double-buffered inputs
   // ws: two record buffers + separate staging; flat: one record buffer aliasing staging
-  static constexpr int BODY = SVK ? (REC_DBL > STG_DBL ? REC_DBL : STG_DBL)
-                                  : 2 * REC_DBL + STG_DBL;
+  static constexpr int BODY = FLAT ? (REC_DBL > STG_DBL ? REC_DBL : STG_DBL)
+                                   : 2 * REC_DBL + STG_DBL;
   static constexpr size_t SMEM = sizeof(double) * ((size_t)HEAD + BODY) + 4 * sizeof(uint64_t);
   static_assert(NS % 2 == 0, "2x2 tiling needs an even number of scalar dofs");
   static_assert(CELLS * (NTILE + 1) <= ACC, "one (cell, tile) per accumulating thread");
@@ -286,8 +289,8 @@ __global__ void __launch_bounds__(PairShape<FEMGPU_ELASTICITY, NS, Q>::THREADS, 
   double* sD = sW + Q;                      // [3][Q][NS]
   double* sP = sD + 3 * Q * NS;             // [Q][4]
   double* sCell = smem + Sh::TAB;           // [CELLS][CELLD]    (producer)
-  double* sIn = sCell + CELLS * Sh::CELLD;  // [CELLS][12] | [CELLS][NCOEF]  (producer)
-  double* sRec = sIn + Sh::IN_DBL;          // [2][REC_DBL]  producer -> consumers
+  double* sIn = sCell + CELLS * Sh::CELLD;  // [2][CELLS][12 | NCOEF]  (producer)
+  double* sRec = sIn + 2 * Sh::IN_DBL;      // [2][REC_DBL]  producer -> consumers
   double* sStg = sRec + 2 * Sh::REC_DBL;    // [CELLS][CSTRIDE]  consumers -> TMA
   uint64_t* full = reinterpret_cast<uint64_t*>(sStg + Sh::STG_DBL);
   uint64_t* empty = full + 2;
@@ -338,21 +341,36 @@ __global__ void __launch_bounds__(PairShape<FEMGPU_ELASTICITY, NS, Q>::THREADS, 
     }
     if (tid == 0) bulk_wait0();
   } else {
-    // ---------------- producers: inputs, geometry, records of tile it ----------------
+    // ---------------- producers: inputs (cp.async, one tile ahead), geometry, records ----
     const int pt = tid - Sh::ACC;
+    auto prefetch = [&](long it) {
+      const long c0 = (blockIdx.x + it * gridDim.x) * CELLS;
+      const int nt = (int)min((long)CELLS, E - c0);
+      double* in = sIn + (it & 1) * Sh::IN_DBL;
+      for (int i = pt; i < nt * 12; i += Sh::PROD) cp_async8(&in[i], coords + c0 * 12 + i);
+      for (int i = pt; i < nt * Sh::NCOEF; i += Sh::PROD)
+        cp_async8(&in[CELLS * 12 + i], coef + c0 * Sh::NCOEF + i);
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    prefetch(0);
     for (long it = 0; it < my_tiles; ++it) {
       const long c0 = (blockIdx.x + it * gridDim.x) * CELLS;
       const int nt = (int)min((long)CELLS, E - c0);
       const int b = (int)(it & 1);
-      for (int i = pt; i < CELLS * 12; i += Sh::PROD) {
-        const int c = i / 12, r = i % 12;  // cells past the end: reference tet
-        sIn[i] = c < nt ? coords[(c0 + c) * 12 + r] : ((r == 3 || r == 7 || r == 11) ? 1.0 : 0.0);
+      const double* in = sIn + b * Sh::IN_DBL;
+      if (it + 1 < my_tiles) {
+        prefetch(it + 1);
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
       }
-      for (int i = pt; i < CELLS * Sh::NCOEF; i += Sh::PROD)
-        sIn[CELLS * 12 + i] = (i / Sh::NCOEF) < nt ? coef[c0 * Sh::NCOEF + i] : 0.0;
       named_bar(2, Sh::PROD);
       if (pt < CELLS) {
-        const Geo g = cell_geometry(&sIn[pt * 12]);
+        double x[12];
+#pragma unroll
+        for (int r = 0; r < 12; ++r)  // cells past the end: reference tet (never stored)
+          x[r] = pt < nt ? in[pt * 12 + r] : ((r == 3 || r == 7 || r == 11) ? 1.0 : 0.0);
+        const Geo g = cell_geometry(x);
         double* cd = sCell + pt * Sh::CELLD;
 #pragma unroll
         for (int a = 0; a < 3; ++a)
@@ -375,12 +393,14 @@ __global__ void __launch_bounds__(PairShape<FEMGPU_ELASTICITY, NS, Q>::THREADS, 
                            K[1 * 3 + bb] * sD[(1 * Q + q) * NS + j] +
                            K[2 * 3 + bb] * sD[(2 * Q + q) * NS + j];
         if (j == 0) {
-          const double* cf = sIn + CELLS * 12 + c * Sh::NCOEF;
+          const double* cf = in + CELLS * 12 + c * Sh::NCOEF;
           double muq = 0, lamq = 0;
+          if (c < nt) {
 #pragma unroll
-          for (int m = 0; m < 4; ++m) {
-            muq += cf[m] * sP[q * 4 + m];
-            lamq += cf[4 + m] * sP[q * 4 + m];
+            for (int m = 0; m < 4; ++m) {
+              muq += cf[m] * sP[q * 4 + m];
+              lamq += cf[4 + m] * sP[q * 4 + m];
+            }
           }
           const double wq = sW[q] * K[9];
           double* qs = qsb + q * Sh::QSD * CELLS + c;
@@ -389,7 +409,7 @@ __global__ void __launch_bounds__(PairShape<FEMGPU_ELASTICITY, NS, Q>::THREADS, 
         }
       }
       mbar_arrive_cta(&full[b]);  // release: this tile's records are visible
-      named_bar(2, Sh::PROD);     // sIn / sCell reused by the next tile
+      named_bar(2, Sh::PROD);     // sIn[b] / sCell reused two tiles later
     }
   }
 }
@@ -397,11 +417,11 @@ __global__ void __launch_bounds__(PairShape<FEMGPU_ELASTICITY, NS, Q>::THREADS, 
 // ============================================================================
 // St Venant-Kirchhoff: flat (all threads in every phase), 2 CTAs per SM
 // ============================================================================
-template <int NS, int Q>
+template <int KIND, int NS, int Q>
 __global__ void __launch_bounds__(128, 2)
     pair_flat_kernel(long E, const double* __restrict__ coords, const double* __restrict__ coef,
                      const double* __restrict__ tab, double* __restrict__ A, int acc) {
-  using Sh = PairShape<FEMGPU_HYPERELASTICITY, NS, Q>;
+  using Sh = PairShape<KIND, NS, Q>;
   constexpr int CELLS = Sh::CELLS;
   extern __shared__ __align__(16) double smem[];
   double* sW = smem;
@@ -409,8 +429,7 @@ __global__ void __launch_bounds__(128, 2)
   double* sP = sD + 3 * Q * NS;             // [Q][4]
   double* sCell = smem + Sh::TAB;           // [CELLS][CELLD]
   double* sIn = sCell + CELLS * Sh::CELLD;  // [CELLS][12] | [CELLS][NCOEF]
-  double* sQd = sIn + Sh::IN_DBL;           // [QC][CELLS][QDD]
-  double* sU = sQd + Sh::QD_DBL;            // records of a chunk / output staging
+  double* sU = sIn + Sh::IN_DBL;            // records of a chunk / output staging
   double* sQs = sU + Sh::QC * NS * Sh::JS;  // [QC][QSD][CELLS]
 
   const int tid = threadIdx.x;
@@ -457,17 +476,36 @@ __global__ void __launch_bounds__(128, 2)
     for (int ch = 0; ch < Sh::NCHUNK; ++ch) {
       const int q0 = ch * Sh::QC;
       const int qn = min(Sh::QC, Q - q0);
-      // ---- per (cell, q): F = I + grad w, w' S, F F^T, lam', mu' ------------
+      // ---- per (cell, q), one thread: F = I + grad w, E, w'S, F F^T, lam', mu',
+      //      then the 10 records g_j, h_j = F g_j, s_j = w' S g_j (F, S in registers)
       for (int task = tid; task < CELLS * qn; task += Sh::THREADS) {
         const int c = task % CELLS, ql = task / CELLS, q = q0 + ql;
         const double* K = sCell + c * Sh::CELLD;
+        constexpr int CO = Sh::SVK ? 3 * NS : 0;  // offset of mu, lam in the dofs
         double muq = 0, lamq = 0;
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
-          muq += coefv(c, 3 * NS + m) * sP[q * 4 + m];
-          lamq += coefv(c, 3 * NS + 4 + m) * sP[q * 4 + m];
+          muq += coefv(c, CO + m) * sP[q * 4 + m];
+          lamq += coefv(c, CO + 4 + m) * sP[q * 4 + m];
         }
         const double wq = sW[q] * K[9];
+        double Kr[9];
+#pragma unroll
+        for (int i = 0; i < 9; ++i) Kr[i] = K[i];
+        double* qs = sQs + ql * Sh::QSD * CELLS + c;
+        qs[0 * CELLS] = lamq * wq;
+        qs[1 * CELLS] = muq * wq;
+        if constexpr (!Sh::SVK) {
+#pragma unroll 2
+          for (int j = 0; j < NS; ++j) {
+            double* rr = sU + (ql * NS + j) * Sh::JS + c;
+#pragma unroll
+            for (int b = 0; b < 3; ++b)
+              rr[b * CELLS] = Kr[0 * 3 + b] * sD[(0 * Q + q) * NS + j] +
+                              Kr[1 * 3 + b] * sD[(1 * Q + q) * NS + j] +
+                              Kr[2 * 3 + b] * sD[(2 * Q + q) * NS + j];
+          }
+        } else {
         double F[3][3];
 #pragma unroll
         for (int cc = 0; cc < 3; ++cc) {
@@ -480,8 +518,8 @@ __global__ void __launch_bounds__(128, 2)
           }
 #pragma unroll
           for (int b = 0; b < 3; ++b)
-            F[cc][b] = (cc == b ? 1.0 : 0.0) + gr[0] * K[0 * 3 + b] + gr[1] * K[1 * 3 + b] +
-                       gr[2] * K[2 * 3 + b];
+            F[cc][b] = (cc == b ? 1.0 : 0.0) + gr[0] * Kr[0 * 3 + b] + gr[1] * Kr[1 * 3 + b] +
+                       gr[2] * Kr[2 * 3 + b];
         }
         double Ee[3][3];
 #pragma unroll
@@ -492,17 +530,12 @@ __global__ void __launch_bounds__(128, 2)
             Ee[a][b] = 0.5 * (a == b ? t - 1.0 : t);
           }
         const double trE = Ee[0][0] + Ee[1][1] + Ee[2][2];
-        double* qd = sQd + (ql * CELLS + c) * Sh::QDD;
+        double Sw[3][3];
 #pragma unroll
         for (int a = 0; a < 3; ++a)
 #pragma unroll
-          for (int b = 0; b < 3; ++b) {
-            qd[a * 3 + b] = F[a][b];
-            qd[9 + a * 3 + b] = wq * ((a == b ? lamq * trE : 0.0) + 2.0 * muq * Ee[a][b]);
-          }
-        double* qs = sQs + ql * Sh::QSD * CELLS + c;
-        qs[0 * CELLS] = lamq * wq;
-        qs[1 * CELLS] = muq * wq;
+          for (int b = 0; b < 3; ++b)
+            Sw[a][b] = wq * ((a == b ? lamq * trE : 0.0) + 2.0 * muq * Ee[a][b]);
         // F F^T: (0,0),(0,1),(0,2),(1,1),(1,2),(2,2)
         qs[2 * CELLS] = F[0][0] * F[0][0] + F[0][1] * F[0][1] + F[0][2] * F[0][2];
         qs[3 * CELLS] = F[0][0] * F[1][0] + F[0][1] * F[1][1] + F[0][2] * F[1][2];
@@ -510,27 +543,22 @@ __global__ void __launch_bounds__(128, 2)
         qs[5 * CELLS] = F[1][0] * F[1][0] + F[1][1] * F[1][1] + F[1][2] * F[1][2];
         qs[6 * CELLS] = F[1][0] * F[2][0] + F[1][1] * F[2][1] + F[1][2] * F[2][2];
         qs[7 * CELLS] = F[2][0] * F[2][0] + F[2][1] * F[2][1] + F[2][2] * F[2][2];
-      }
-      __syncthreads();
-      // ---- records of the chunk: per (cell, q, j): g, h = F g, s = w' S g ----
-      for (int task = tid; task < CELLS * qn * NS; task += Sh::THREADS) {
-        const int c = task % CELLS, r = task / CELLS;
-        const int j = r % NS, ql = r / NS, q = q0 + ql;
-        const double* K = sCell + c * Sh::CELLD;
-        double g[3];
+#pragma unroll 2
+        for (int j = 0; j < NS; ++j) {
+          double g[3];
 #pragma unroll
-        for (int b = 0; b < 3; ++b)
-          g[b] = K[0 * 3 + b] * sD[(0 * Q + q) * NS + j] + K[1 * 3 + b] * sD[(1 * Q + q) * NS + j] +
-                 K[2 * 3 + b] * sD[(2 * Q + q) * NS + j];
-        double* rr = sU + (ql * NS + j) * Sh::JS + c;
-        const double* qd = sQd + (ql * CELLS + c) * Sh::QDD;
+          for (int b = 0; b < 3; ++b)
+            g[b] = Kr[0 * 3 + b] * sD[(0 * Q + q) * NS + j] + Kr[1 * 3 + b] * sD[(1 * Q + q) * NS + j] +
+                   Kr[2 * 3 + b] * sD[(2 * Q + q) * NS + j];
+          double* rr = sU + (ql * NS + j) * Sh::JS + c;
 #pragma unroll
-        for (int b = 0; b < 3; ++b) rr[b * CELLS] = g[b];
+          for (int b = 0; b < 3; ++b) rr[b * CELLS] = g[b];
 #pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          rr[(3 + a) * CELLS] = qd[a * 3 + 0] * g[0] + qd[a * 3 + 1] * g[1] + qd[a * 3 + 2] * g[2];
-          rr[(6 + a) * CELLS] =
-              qd[9 + a * 3 + 0] * g[0] + qd[9 + a * 3 + 1] * g[1] + qd[9 + a * 3 + 2] * g[2];
+          for (int a = 0; a < 3; ++a) {
+            rr[(3 + a) * CELLS] = F[a][0] * g[0] + F[a][1] * g[1] + F[a][2] * g[2];
+            rr[(6 + a) * CELLS] = Sw[a][0] * g[0] + Sw[a][1] * g[1] + Sw[a][2] * g[2];
+          }
+        }
         }
       }
       __syncthreads();
@@ -555,7 +583,7 @@ template <int KIND, int NS, int Q>
 static cudaError_t launch_pair_t(long E, const double* coords, const double* coef,
                                  const double* tab, double* A, int acc, cudaStream_t s) {
   using Sh = PairShape<KIND, NS, Q>;
-  auto kern = Sh::SVK ? pair_flat_kernel<NS, Q> : pair_ws_kernel<NS, Q>;
+  auto kern = (Sh::SVK || Sh::FLAT) ? pair_flat_kernel<KIND, NS, Q> : pair_ws_kernel<NS, Q>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e =
