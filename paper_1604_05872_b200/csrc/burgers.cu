@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(256, 1)
         //   jj = 2h + t/2, kk = 2(t%2) + e
 #pragma unroll
         for (int vh = 0; vh < 2; ++vh) {
-          if (!(vh ? row_ok1 : row_ok0)) continue;
+          const bool ok = vh ? row_ok1 : row_ok0;  // lane-pair uniform (same g)
           double* Ae = A + (c0 + g + 8 * vh) * (size_t)N * N;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
@@ -354,20 +354,33 @@ __global__ void __launch_bounds__(256, 1)
               double2 vd = make_double2(m[0] + (dg ? cdir[h][2 * vh] : 0.0),
                                         m[1] + (dg ? cdir[h][2 * vh + 1] : 0.0));
               double2* pd = reinterpret_cast<double2*>(Ae + (c * NS + j) * N + d * NS + k);
-              if (acc) {
-                const double2 o = *pd;
-                vd.x += o.x;
-                vd.y += o.y;
+              if (ok) {
+                if (acc) {
+                  const double2 o = *pd;
+                  vd.x += o.x;
+                  vd.y += o.y;
+                }
+                stg_stream(pd, vd);
               }
-              stg_stream(pd, vd);
               if (mirror) {
-                // mirror: rows (c, k+e), column (d, j); C part = C_{k+e, j}
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                  double* pm = Ae + (c * NS + k + e) * N + d * NS + j;
-                  double vm = m[e] + (dg ? cmir[h][2 * vh + e] : 0.0);
-                  if (acc) vm += *pm;
-                  stg64(pm, vm);
+                // mirror: rows (c, k+e), column (d, j); C part = C_{k+e, j}.  Lanes
+                // t and t^2 hold columns j, j+1 of rows k, k+1: swap one value so
+                // each lane stores a 16-byte row segment.
+                const double vm0 = m[0] + (dg ? cmir[h][2 * vh] : 0.0);
+                const double vm1 = m[1] + (dg ? cmir[h][2 * vh + 1] : 0.0);
+                const bool lo = (t >> 1) == 0;
+                const double other = __shfl_xor_sync(0xffffffffu, lo ? vm1 : vm0, 2);
+                const int jj0 = 4 * J + 2 * h;  // even column of the pair
+                double2* pm = reinterpret_cast<double2*>(
+                    Ae + (c * NS + k + (lo ? 0 : 1)) * N + d * NS + jj0);
+                double2 vmv = lo ? make_double2(vm0, other) : make_double2(other, vm1);
+                if (ok) {
+                  if (acc) {
+                    const double2 o = *pm;
+                    vmv.x += o.x;
+                    vmv.y += o.y;
+                  }
+                  stg_stream(pm, vmv);
                 }
               }
             }
