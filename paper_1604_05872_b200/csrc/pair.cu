@@ -60,7 +60,7 @@ struct PairShape {
   static constexpr int THREADS = ACC + PROD;
   static constexpr int CTAS_PER_SM = 2;
   static constexpr int NCOEF = SVK ? 3 * NS + 8 : 8;
-  static constexpr int QC = SVK ? 9 : Q;                 // quadrature points per chunk
+  static constexpr int QC = SVK ? 14 : Q;                // quadrature points per chunk (SVK: 14 -> 112 of 128 threads busy in the setup phase)
   static constexpr int NCHUNK = (Q + QC - 1) / QC;
   static constexpr int RECD = SVK ? 9 : 3;               // per (q,j): g | h | s
   static constexpr int QSD = SVK ? 8 : 2;                // per q: lam', mu' | F F^T (6)
