@@ -7,26 +7,41 @@
 //
 // femopt cannot optimize the monolithic IR (exact cover limit, sharing.cpp:355,
 // SURVEY.md App. A P5); per component block it pre-evaluates part of the
-// monomials (P14: ~0.91 M flops/cell).  Here the whole Jacobian is a TENSOR
-// schedule (pre-evaluation, preeval.cpp:279-451) factored into two FP64
-// tensor-core GEMMs per 16-cell tile (mma.sync m16n8k4 f64 -> DMMA):
+// monomials (P14: ~0.91 M flops/cell).  Here the Jacobian is a TENSOR schedule
+// (pre-evaluation, preeval.cpp:279-451) factored into two FP64 tensor-core
+// GEMMs per 16-cell tile (mma.sync m16n8k4 f64 -> DMMA):
 //
-//  GEMM-1 (per component c):  H^{c,a}_{jk} = sum_n u_{c,n} T^{n,a}_{jk}
-//         T^{n,a}_{jk} = sum_q W D_a(phi_n) phi_j phi_k  (resident in smem)
-//         M^{cd}_{jk} = |det| sum_a K_ad H^{c,a}_{jk}   (reference -> physical)
-//  GEMM-2 (once):             C_{jk} = sum_alpha g_alpha R_{alpha,jk}
+//  GEMM-1 (per (c,d)):  M^{cd}_{jk} = sum_m g^{cd}_m S_{m,jk}
+//         The reference derivative tables D_a span the derivative space of
+//         the element (P2 for P3: rank r = 10 <= 12) at the quadrature
+//         points.  With an orthonormal basis Psi (Q x r) of that span,
+//         D_a = Psi Dn_a exactly, so d_d u_c(x_q) = sum_m Psi_qm g^{cd}_m,
+//         g^{cd}_m = |det| sum_a K_ad (Dn_a u_c)_m   (per cell, CUDA cores)
+//         S_{m,jk}  = sum_q W_q Psi_qm phi_j(q) phi_k(q)   (host, once)
+//  GEMM-2 (once):       C_{jk} = sum_alpha g_alpha R_{alpha,jk}
 //         alpha = (n,a): |det| sum_b u_{b,n} K_ab  x  sum_q W phi_n phi_j D_a(phi_k)
 //                 s:     |det| nu (K K^T)_s       x  sum_q W D_a phi_j D_b phi_k (+ sym)
 //                 mass:  |det| / dt               x  sum_q W phi_j phi_k
-//         (B fragments through a 4-deep TMA bulk-copy ring, mbarrier full/empty)
 //
-// Output layout without staging: the 20x20 (j,k) plane is cut into 4x4
-// blocks; a warp owns whole upper blocks (J<=K).  An n8 fragment covers two
-// block rows, so every lane holds a 16-byte row segment and lane pairs form
-// full 32-byte sectors of A_e.  The mirror block (K,J) reuses the same
-// registers (M is symmetric); its C part comes from GEMM-2 columns permuted so
-// that C_{kj} lands in the lane that writes position (k,j).  No shuffles, no
-// shared-memory staging, no block-level synchronisation inside a tile.
+// Work split: the 20x20 (j,k) plane is cut into 4x4 blocks; the 15 upper
+// blocks (J <= K) belong to warps 0..14 of a 16-warp CTA (one CTA per SM).
+// Each warp keeps its block's S fragments in registers for the whole kernel,
+// computes the block's C (direct + permuted mirror tiles, B fragments from L2)
+// once per tile, then for each of the 9 (c,d) blocks of A_e: 6 DMMAs, + C on
+// the diagonal, and writes the 4x4 block and its mirror into a shared-memory
+// slab [16 cells][20][20].  Warp 15 issues one 3D TMA tensor store per slab
+// (box 20 x 20 x 16 cells, clipped at E; cp.reduce...add for accumulate) and
+// keeps three slabs in flight, so HBM sees long, full-line write streams while
+// the tensor cores work on the next block.  The element matrix (28.8 KB/cell)
+// is written exactly once: this form is HBM-write bound.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <mutex>
+#include <vector>
+
 #include "common.cuh"
 #include "femgpu_internal.h"
 
@@ -36,31 +51,24 @@ namespace bz {
 constexpr int NS = 20;
 constexpr int N = 60;
 constexpr int NBU = 15;            // upper 4x4 blocks (J <= K) of the 20x20 (j,k) plane
-constexpr int NT1 = 3 * NBU * 2;   // GEMM-1 n8 tiles: (a, upper block, half)
-constexpr int KS1 = 5;             // GEMM-1 k4 steps (n = 0..19)
+constexpr int KS1 = 3;             // GEMM-1 k4 steps over the derivative space
+constexpr int RMAX = 4 * KS1;      // largest supported derivative-space rank
 constexpr int KS2 = 18;            // GEMM-2 k4 steps: 60 (n,a) + 6 (G) + 1 (mass) + pad
-constexpr int KPS2 = 3;            // k4 steps per ring stage
-constexpr int NST2 = KS2 / KPS2;   // ring stages per pass
-constexpr int NT2 = 50;            // GEMM-2 n8 tiles: 15 direct + 10 mirror blocks, x2 halves
 constexpr int CELLS = 16;
-constexpr int THREADS = 256;
-constexpr int WARPS = 8;
-constexpr int T1_DBL = KS1 * NT1 * 32;         // 14400
-constexpr int R2_DBL = KS2 * NT2 * 32;         // 27200
-constexpr int A1_DBL = 3 * KS1 * 64;           // u_c fragments
-constexpr int A2_DBL = KS2 * 64;               // g2 fragments
-constexpr int IN_DBL = CELLS * (12 + 3 * NS);  // coords | u (cp.async target)
-constexpr int CELLD = 10;                      // K(9), adet
-// GEMM-2 B operand: TMA ring of per-k-step stages.  A tile runs two passes (the
-// first and second block of every warp); pass p's stage holds only the n8
-// tiles its warps need (30 resp. 20), laid out contiguously on the host.
-constexpr int NB = 3;                          // ring depth
-constexpr int SLOTS0 = 30, SLOTS1 = 20;
-constexpr int STAGE_MAX = KPS2 * SLOTS0 * 32;  // doubles
-constexpr int R2_OFF1 = KS2 * SLOTS0 * 32;     // pass-1 offset inside the R2 table
-constexpr size_t SMEM = sizeof(double) * (size_t)(T1_DBL + A1_DBL + A2_DBL + IN_DBL +
-                                                  CELLS * CELLD + NB * STAGE_MAX) +
-                        2 * NB * sizeof(uint64_t);
+constexpr int WARPS = 16;
+constexpr int THREADS = 32 * WARPS;
+constexpr int ISSUER = WARPS - 1;  // warp without a block: TMA stores
+constexpr int NSLAB = 3;
+constexpr int SLAB_DBL = CELLS * NS * NS;     // one (c,d) block of 16 cells
+constexpr int S_DBL = NBU * KS1 * 2 * 32;     // GEMM-1 B fragments
+constexpr int R2_DBL = NBU * KS2 * 4 * 32;    // GEMM-2 B fragments
+constexpr int DN_DBL = 3 * RMAX * NS;         // Dn_a (r x 20), zero rows past r
+constexpr int A1_DBL = 9 * KS1 * 64;          // g^{cd} fragments
+constexpr int A2_DBL = KS2 * 64;              // GEMM-2 A fragments
+constexpr int IN_DBL = CELLS * (12 + 3 * NS); // coords | u (cp.async target)
+constexpr int CELLD = 10;                     // K(9), adet
+constexpr size_t SMEM =
+    sizeof(double) * (size_t)(NSLAB * SLAB_DBL + DN_DBL + A1_DBL + A2_DBL + IN_DBL + CELLS * CELLD);
 }  // namespace bz
 
 // Upper block u (row-major over J <= K) -> (J, K).
@@ -70,34 +78,11 @@ __host__ __device__ constexpr int bz_J(int u) {
 __host__ __device__ constexpr int bz_K(int u) {
   return u < 5 ? u : u < 9 ? u - 4 : u < 12 ? u - 7 : u < 14 ? u - 9 : 4;
 }
-// Off-diagonal upper blocks in order get GEMM-2 mirror slots 0..9.
-__host__ __device__ constexpr int bz_mirror_slot(int u) {
-  return bz_J(u) == bz_K(u) ? -1 : u - (bz_J(u) + 1);
-}
 
-// Warp work lists (upper blocks), balanced for GEMM-1 + GEMM-2 cost per SM
-// sub-partition (warps w and w+4 share one).  Warp 7 (one block only) doubles
-// as the TMA producer of the GEMM-2 ring.
-constexpr int kWblk[bz::WARPS][2] = {{0, 5}, {1, 9}, {2, 12}, {3, 14}, {4, 6},
-                                     {7, 8}, {10, 11}, {13, -1}};
-__constant__ int c_wblk[bz::WARPS][2] = {{0, 5}, {1, 9}, {2, 12}, {3, 14}, {4, 6},
-                                         {7, 8}, {10, 11}, {13, -1}};
-// first GEMM-2 slot of warp w in pass p (direct h0, h1, then mirror h0, h1)
-constexpr int bz_slot_base(int w, int p) {
-  int off = 0;
-  for (int x = 0; x < w; ++x) {
-    const int ub = kWblk[x][p];
-    if (ub >= 0) off += (bz_J(ub) == bz_K(ub)) ? 2 : 4;
-  }
-  return off;
-}
-__constant__ int c_slot[bz::WARPS][2] = {
-    {bz_slot_base(0, 0), bz_slot_base(0, 1)}, {bz_slot_base(1, 0), bz_slot_base(1, 1)},
-    {bz_slot_base(2, 0), bz_slot_base(2, 1)}, {bz_slot_base(3, 0), bz_slot_base(3, 1)},
-    {bz_slot_base(4, 0), bz_slot_base(4, 1)}, {bz_slot_base(5, 0), bz_slot_base(5, 1)},
-    {bz_slot_base(6, 0), bz_slot_base(6, 1)}, {bz_slot_base(7, 0), bz_slot_base(7, 1)}};
-static_assert(bz_slot_base(bz::WARPS, 0) == bz::SLOTS0, "pass-0 slot count");
-static_assert(bz_slot_base(bz::WARPS, 1) == bz::SLOTS1, "pass-1 slot count");
+// Warp -> upper block.  Sub-partition s runs warps s, s+4, s+8, s+12; the ten
+// off-diagonal blocks (GEMM-2: 72 DMMA/tile) and five diagonal ones (36) are
+// spread so that no sub-partition carries more than 3 off + 1 diagonal.
+__constant__ int c_wblk[bz::WARPS] = {1, 2, 3, 4, 6, 7, 8, 10, 11, 13, 0, 5, 9, 12, 14, -1};
 
 __device__ __forceinline__ void dmma16x8x4(double (&c)[4], double a0, double a1, double b) {
   asm volatile(
@@ -109,7 +94,7 @@ __device__ __forceinline__ void dmma16x8x4(double (&c)[4], double a0, double a1,
 
 __device__ __forceinline__ double ldg_nc(const double* p) {
   double v;
-  asm volatile("ld.global.nc.f64 %0, [%1];\n" : "=d"(v) : "l"(p));
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];\n" : "=d"(v) : "l"(p));
   return v;
 }
 
@@ -117,72 +102,60 @@ __device__ __forceinline__ void cp_async8b(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 
-__device__ __forceinline__ void mbar_arrive_cta_bz(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+__device__ __forceinline__ void slab_store(const CUtensorMap* map, const double* src, int col,
+                                           int row, int cell, int acc) {
+  if (acc)
+    asm volatile(
+        "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group "
+        "[%0, {%1, %2, %3}], [%4];\n" ::"l"(map),
+        "r"(col), "r"(row), "r"(cell), "r"(smem_u32(src))
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(
+            map),
+        "r"(col), "r"(row), "r"(cell), "r"(smem_u32(src))
+        : "memory");
 }
 
-__device__ __forceinline__ void stg64(double* p, double v) {
-  asm volatile("st.global.cs.f64 [%0], %1;\n" ::"l"(p), "d"(v) : "memory");
+__device__ __forceinline__ void bulk_wait_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
 }
 
-__global__ void __launch_bounds__(256, 1)
-    burgers_kernel(long E, const double* __restrict__ coords, const double* __restrict__ u,
-                   const double* __restrict__ tab, double nu, double dt,
-                   double* __restrict__ A, int acc) {
+__global__ void __launch_bounds__(bz::THREADS, 1)
+    burgers_kernel(const __grid_constant__ CUtensorMap amap, long E,
+                   const double* __restrict__ coords, const double* __restrict__ u,
+                   const double* __restrict__ tab, double nu, double dt, int acc) {
   using namespace bz;
-  extern __shared__ __align__(16) double smem[];
-  double* sT1 = smem;                   // [KS1][NT1][32]  (m16n8k4 B fragments)
-  double* sA1 = sT1 + T1_DBL;           // [3][KS1][32][2]
-  double* sA2 = sA1 + A1_DBL;           // [KS2][32][2]
-  double* sIn = sA2 + A2_DBL;           // [CELLS][12] | [CELLS][60]
-  double* sCell = sIn + IN_DBL;         // [CELLS][10]
-  double* sRing = sCell + CELLS * CELLD;  // [NB][STAGE_MAX]  GEMM-2 B stages
-  uint64_t* rFull = reinterpret_cast<uint64_t*>(sRing + NB * STAGE_MAX);
-  uint64_t* rEmpty = rFull + NB;
-  const double* gR2 = tab + T1_DBL;     // [pass][KS2][slots][32]
+  extern __shared__ __align__(1024) double smem[];
+  double* sSlab = smem;                    // [NSLAB][CELLS][20][20]  (TMA box layout)
+  double* sDn = sSlab + NSLAB * SLAB_DBL;  // [3][RMAX][20]
+  double* sA1 = sDn + DN_DBL;              // [9][KS1][32][2]
+  double* sA2 = sA1 + A1_DBL;              // [KS2][32][2]
+  double* sIn = sA2 + A2_DBL;              // [CELLS][12] | [CELLS][60]
+  double* sCell = sIn + IN_DBL;            // [CELLS][10]
+  const double* gS = tab;                  // [ub][KS1][2][32]
+  const double* gR2 = tab + S_DBL;         // [ub][KS2][4][32]
+  const double* gDn = gR2 + R2_DBL;        // [3][RMAX][20]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
+  const int ub = c_wblk[warp];
+  const int J = ub >= 0 ? bz_J(ub) : 0, K = ub >= 0 ? bz_K(ub) : 0;
+  const bool mirror = J != K;
+  const bool issuer = warp == ISSUER && lane == 0;
+  const int hs = g & 1;  // odd-g lanes write the other half first (bank spread)
 
-  for (int i = tid; i < T1_DBL / 2; i += THREADS)
-    reinterpret_cast<double2*>(sT1)[i] = reinterpret_cast<const double2*>(tab)[i];
+  for (int i = tid; i < DN_DBL; i += THREADS) sDn[i] = gDn[i];
+  // GEMM-1 B fragments of this warp's block: registers for the whole kernel
+  double sb[KS1][2];
+#pragma unroll
+  for (int ks = 0; ks < KS1; ++ks)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      sb[ks][h] = ub >= 0 ? gS[((ub * KS1 + ks) * 2 + h) * 32 + lane] : 0.0;
 
   const long ntiles = (E + CELLS - 1) / CELLS;
-  const long my_tiles =
-      (long)blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  const long total_stages = my_tiles * 2 * NST2;
-  const bool producer = (warp == WARPS - 1) && lane == 0;
-  auto issue_stage = [&](long gs) {  // stage gs -> ring slot gs % NB
-    const int b = (int)(gs % NB);
-    const int pass = (int)((gs / NST2) & 1), st = (int)(gs % NST2);
-    const int slots = pass ? SLOTS1 : SLOTS0;
-    const double* src = gR2 + (pass ? R2_OFF1 : 0) + (size_t)st * KPS2 * slots * 32;
-    mbar_expect_tx(&rFull[b], KPS2 * slots * 32 * 8);
-    bulk_g2s(sRing + b * STAGE_MAX, src, KPS2 * slots * 32 * 8, &rFull[b]);
-  };
-  if (tid == 0) {
-    for (int b = 0; b < NB; ++b) {
-      mbar_init(&rFull[b], 1);
-      mbar_init(&rEmpty[b], WARPS);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (producer)
-    for (long gs = 0; gs < NB && gs < total_stages; ++gs) issue_stage(gs);
-  // consume stage gs (wait full), release it, and (producer) refill the slot
-  auto stage_wait = [&](long gs) {
-    mbar_wait(&rFull[gs % NB], (uint32_t)((gs / NB) & 1));
-  };
-  auto stage_release = [&](long gs) {
-    __syncwarp();
-    if (lane == 0) mbar_arrive_cta_bz(&rEmpty[gs % NB]);
-    if (producer && gs + NB < total_stages) {
-      mbar_wait(&rEmpty[gs % NB], (uint32_t)((gs / NB) & 1));
-      issue_stage(gs + NB);
-    }
-  };
-  long it = -1;
   auto prefetch = [&](long tile) {
     const long c0 = tile * CELLS;
     const int nt = (int)min((long)CELLS, E - c0);
@@ -193,12 +166,12 @@ __global__ void __launch_bounds__(256, 1)
   };
   if ((long)blockIdx.x < ntiles) prefetch(blockIdx.x);
 
+  long gi = 0;  // running (c,d) block counter of this CTA: slab gi % NSLAB
   for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    ++it;
     const long c0 = tile * CELLS;
     const int nt = (int)min((long)CELLS, E - c0);
     asm volatile("cp.async.wait_all;\n" ::: "memory");
-    __syncthreads();  // inputs landed; previous tile's readers of sA1/sA2/sCell done
+    __syncthreads();  // inputs landed; previous tile's readers of sA1/sA2 done
     if (tid < CELLS) {
       double x[12];
 #pragma unroll
@@ -213,13 +186,27 @@ __global__ void __launch_bounds__(256, 1)
       cd[9] = geo.adet;
     }
     __syncthreads();
-    // ---- A fragments: u_c (GEMM-1) and g2 (GEMM-2); a[v] = A[g + 8v][t] ----
-    for (int i = tid; i < 3 * KS1 * 64; i += THREADS) {
-      const int c = i / (KS1 * 64), r = i % (KS1 * 64);
-      const int ks = r / 64, ln = (r % 64) / 2, v = r % 2;
-      const int cell = (ln >> 2) + 8 * v, n = ks * 4 + (ln & 3);
-      sA1[i] = cell < nt ? sIn[CELLS * 12 + cell * 3 * NS + c * NS + n] : 0.0;
+    // ---- GEMM-1 A: g^{cd}_m = |det| sum_a K_ad (Dn_a u_c)_m; a[v] = A[g+8v][t] ----
+    for (int i = tid; i < CELLS * 3 * RMAX; i += THREADS) {
+      const int cell = i / (3 * RMAX), c = (i / RMAX) % 3, m = i % RMAX;
+      double gu[3] = {0.0, 0.0, 0.0};
+      if (cell < nt) {
+        const double* uc = sIn + CELLS * 12 + cell * 3 * NS + c * NS;
+#pragma unroll 4
+        for (int n = 0; n < NS; ++n) {
+          const double un = uc[n];
+#pragma unroll
+          for (int a = 0; a < 3; ++a) gu[a] = fma(sDn[(a * RMAX + m) * NS + n], un, gu[a]);
+        }
+      }
+      const double* cd = sCell + cell * CELLD;
+      const int ks = m >> 2, ln = 4 * (cell & 7) + (m & 3), v = cell >> 3;
+#pragma unroll
+      for (int d = 0; d < 3; ++d)
+        sA1[(((c * 3 + d) * KS1 + ks) * 32 + ln) * 2 + v] =
+            cd[9] * (cd[0 * 3 + d] * gu[0] + cd[1 * 3 + d] * gu[1] + cd[2 * 3 + d] * gu[2]);
     }
+    // ---- GEMM-2 A fragments ----
     for (int i = tid; i < KS2 * 64; i += THREADS) {
       const int ks = i / 64, ln = (i % 64) / 2, v = i % 2;
       const int cell = (ln >> 2) + 8 * v, al = ks * 4 + (ln & 3);
@@ -247,154 +234,114 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();
     if (tile + gridDim.x < ntiles) prefetch(tile + gridDim.x);
 
-    // per-lane cell data for rows g and g+8
-    double Kc[2][9], ad[2];
+    // ---- GEMM-2: C direct (tiles 0,1) and mirror (2,3); B from L2 ----------
+    double cdir[2][4], cmir[2][4];
 #pragma unroll
-    for (int vh = 0; vh < 2; ++vh) {
-      const double* cd = sCell + (g + 8 * vh) * CELLD;
+    for (int h = 0; h < 2; ++h)
 #pragma unroll
-      for (int i = 0; i < 9; ++i) Kc[vh][i] = cd[i];
-      ad[vh] = cd[9];
+      for (int v = 0; v < 4; ++v) cdir[h][v] = cmir[h][v] = 0.0;
+    if (ub >= 0) {
+      const double* r2 = gR2 + (size_t)ub * KS2 * 4 * 32 + lane;
+      constexpr int CH = 3;  // k4 steps per register chunk (double-buffered)
+      double bq[2][CH][4];
+#pragma unroll
+      for (int kk = 0; kk < CH; ++kk)
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+          bq[0][kk][x] = (x < 2 || mirror) ? ldg_nc(r2 + (kk * 4 + x) * 32) : 0.0;
+#pragma unroll
+      for (int ch = 0; ch < KS2 / CH; ++ch) {
+        const int cur = ch & 1;
+        if (ch + 1 < KS2 / CH) {
+#pragma unroll
+          for (int kk = 0; kk < CH; ++kk)
+#pragma unroll
+            for (int x = 0; x < 4; ++x)
+              bq[cur ^ 1][kk][x] =
+                  (x < 2 || mirror) ? ldg_nc(r2 + (((ch + 1) * CH + kk) * 4 + x) * 32) : 0.0;
+        }
+#pragma unroll
+        for (int kk = 0; kk < CH; ++kk) {
+          const double2 af = reinterpret_cast<const double2*>(sA2)[(ch * CH + kk) * 32 + lane];
+          dmma16x8x4(cdir[0], af.x, af.y, bq[cur][kk][0]);
+          dmma16x8x4(cdir[1], af.x, af.y, bq[cur][kk][1]);
+          if (mirror) {
+            dmma16x8x4(cmir[0], af.x, af.y, bq[cur][kk][2]);
+            dmma16x8x4(cmir[1], af.x, af.y, bq[cur][kk][3]);
+          }
+        }
+      }
     }
-    const bool row_ok0 = g < nt, row_ok1 = g + 8 < nt;
 
+    // ---- the nine (c,d) blocks: GEMM-1, + C on the diagonal, slab, TMA ----
 #pragma unroll 1
-    for (int wb = 0; wb < 2; ++wb) {
-      const int ub = c_wblk[warp][wb];
-      const long gs0 = (it * 2 + wb) * NST2;  // first ring stage of this pass
-      if (ub < 0) {  // no block in this pass: keep the ring moving
-#pragma unroll 1
-        for (int st = 0; st < NST2; ++st) {
-          stage_wait(gs0 + st);
-          stage_release(gs0 + st);
-        }
-        continue;
-      }
-      const int J = bz_J(ub), K = bz_K(ub);
-      const int ms = bz_mirror_slot(ub);
-      const bool mirror = ms >= 0;
-      // ---- GEMM-2: C direct (tiles 2ub, 2ub+1) and mirror (30 + 2ms + h) ----
-      double cdir[2][4], cmir[2][4];
+    for (int cdi = 0; cdi < 9; ++cdi, ++gi) {
+      const int c = cdi / 3, d = cdi % 3;
+      double* slab = sSlab + (gi % NSLAB) * SLAB_DBL;
+      if (ub >= 0) {
+        double m[2][4];
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
+        for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) cdir[h][v] = cmir[h][v] = 0.0;
-      {
-        const int slot = c_slot[warp][wb];
-        const int slots = wb ? SLOTS1 : SLOTS0;
-#pragma unroll 1
-        for (int st = 0; st < NST2; ++st) {
-          const long gs = gs0 + st;
-          stage_wait(gs);
-          const double* stb = sRing + (gs % NB) * STAGE_MAX + slot * 32 + lane;
-          double bq[KPS2][4];
-          double2 aq[KPS2];
-#pragma unroll
-          for (int kk = 0; kk < KPS2; ++kk) {  // all operand loads of the stage first
-            const double* p = stb + kk * slots * 32;
-            bq[kk][0] = p[0];
-            bq[kk][1] = p[32];
-            bq[kk][2] = mirror ? p[64] : 0.0;
-            bq[kk][3] = mirror ? p[96] : 0.0;
-            aq[kk] = reinterpret_cast<const double2*>(sA2)[(st * KPS2 + kk) * 32 + lane];
-          }
-          stage_release(gs);
-#pragma unroll
-          for (int kk = 0; kk < KPS2; ++kk) {
-            dmma16x8x4(cdir[0], aq[kk].x, aq[kk].y, bq[kk][0]);
-            dmma16x8x4(cdir[1], aq[kk].x, aq[kk].y, bq[kk][1]);
-            if (mirror) {
-              dmma16x8x4(cmir[0], aq[kk].x, aq[kk].y, bq[kk][2]);
-              dmma16x8x4(cmir[1], aq[kk].x, aq[kk].y, bq[kk][3]);
-            }
-          }
-        }
-      }
-      // ---- GEMM-1 per component c, then direct + mirror stores ------------
-      // (unrolled: the delta_cd selection of C is resolved at compile time)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        double hacc[3][2][4];
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int v = 0; v < 4; ++v) hacc[a][h][v] = 0.0;
+          for (int v = 0; v < 4; ++v) m[h][v] = 0.0;
 #pragma unroll
         for (int ks = 0; ks < KS1; ++ks) {
-          const double2 af = reinterpret_cast<const double2*>(sA1)[(c * KS1 + ks) * 32 + lane];
-#pragma unroll
-          for (int a = 0; a < 3; ++a)
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-              dmma16x8x4(hacc[a][h], af.x, af.y,
-                         sT1[(ks * NT1 + (a * NBU + ub) * 2 + h) * 32 + lane]);
+          const double2 af = reinterpret_cast<const double2*>(sA1)[(cdi * KS1 + ks) * 32 + lane];
+          dmma16x8x4(m[0], af.x, af.y, sb[ks][0]);
+          dmma16x8x4(m[1], af.x, af.y, sb[ks][1]);
         }
-        // positions: row (cell g + 8vh), column pair e = 0,1 of tile h:
-        //   jj = 2h + t/2, kk = 2(t%2) + e
+        const double dg = c == d ? 1.0 : 0.0;
+        // C fragment c[v] = C[cell g + 8(v>>1)][col 2t + (v&1)];
+        // col -> (j, k) = (4J + 2h + t/2, 4K + 2(t&1) + e)
 #pragma unroll
-        for (int vh = 0; vh < 2; ++vh) {
-          const bool ok = vh ? row_ok1 : row_ok0;  // lane-pair uniform (same g)
-          double* Ae = A + (c0 + g + 8 * vh) * (size_t)N * N;
+        for (int hi = 0; hi < 2; ++hi) {
+          const int h = hi ^ hs;
+          double dv[4], rv[4];
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int j = 4 * J + 2 * h + (t >> 1);
-            const int k = 4 * K + 2 * (t & 1);
+          for (int v = 0; v < 4; ++v) {
+            const double mv = hs ? m[hi ^ 1][v] : m[hi][v];
+            dv[v] = fma(dg, hs ? cdir[hi ^ 1][v] : cdir[hi][v], mv);
+            rv[v] = fma(dg, hs ? cmir[hi ^ 1][v] : cmir[hi][v], mv);
+          }
+          const int j = 4 * J + 2 * h + (t >> 1);
+          const int k = 4 * K + 2 * (t & 1);
 #pragma unroll
-            for (int d = 0; d < 3; ++d) {
-              double m[2];
-#pragma unroll
-              for (int e = 0; e < 2; ++e)
-                m[e] = ad[vh] * (Kc[vh][0 * 3 + d] * hacc[0][h][2 * vh + e] +
-                                 Kc[vh][1 * 3 + d] * hacc[1][h][2 * vh + e] +
-                                 Kc[vh][2 * 3 + d] * hacc[2][h][2 * vh + e]);
-              const bool dg = (c == d);
-              // direct: row (c, j), columns (d, k..k+1) -- 16 B, lane pairs fill a sector
-              double2 vd = make_double2(m[0] + (dg ? cdir[h][2 * vh] : 0.0),
-                                        m[1] + (dg ? cdir[h][2 * vh + 1] : 0.0));
-              double2* pd = reinterpret_cast<double2*>(Ae + (c * NS + j) * N + d * NS + k);
-              if (ok) {
-                if (acc) {
-                  const double2 o = *pd;
-                  vd.x += o.x;
-                  vd.y += o.y;
-                }
-                stg_stream(pd, vd);
-              }
-              if (mirror) {
-                // mirror: rows (c, k+e), column (d, j); C part = C_{k+e, j}.  Lanes
-                // t and t^2 hold columns j, j+1 of rows k, k+1: swap one value so
-                // each lane stores a 16-byte row segment.
-                const double vm0 = m[0] + (dg ? cmir[h][2 * vh] : 0.0);
-                const double vm1 = m[1] + (dg ? cmir[h][2 * vh + 1] : 0.0);
-                const bool lo = (t >> 1) == 0;
-                const double other = __shfl_xor_sync(0xffffffffu, lo ? vm1 : vm0, 2);
-                const int jj0 = 4 * J + 2 * h;  // even column of the pair
-                double2* pm = reinterpret_cast<double2*>(
-                    Ae + (c * NS + k + (lo ? 0 : 1)) * N + d * NS + jj0);
-                double2 vmv = lo ? make_double2(vm0, other) : make_double2(other, vm1);
-                if (ok) {
-                  if (acc) {
-                    const double2 o = *pm;
-                    vmv.x += o.x;
-                    vmv.y += o.y;
-                  }
-                  stg_stream(pm, vmv);
-                }
-              }
+          for (int vh = 0; vh < 2; ++vh) {
+            double* cellp = slab + (g + 8 * vh) * (NS * NS);
+            *reinterpret_cast<double2*>(cellp + j * NS + k) =
+                make_double2(dv[2 * vh], dv[2 * vh + 1]);
+            if (mirror) {
+              // mirror: rows k+e, column j.  Lanes t and t^2 hold columns j, j+1
+              // of rows k, k+1: swap one value so each lane writes 16 bytes.
+              const bool lo = (t >> 1) == 0;
+              const double other =
+                  __shfl_xor_sync(0xffffffffu, lo ? rv[2 * vh + 1] : rv[2 * vh], 2);
+              const int jj0 = 4 * J + 2 * h;
+              *reinterpret_cast<double2*>(cellp + (k + (lo ? 0 : 1)) * NS + jj0) =
+                  lo ? make_double2(rv[2 * vh], other) : make_double2(other, rv[2 * vh + 1]);
             }
           }
         }
+      }
+      fence_proxy_async();  // generic-proxy slab writes -> visible to the TMA unit
+      if (issuer) bulk_wait_read1();  // slab of block gi-2 free before anyone writes it next
+      __syncthreads();
+      if (issuer) {
+        slab_store(&amap, slab, d * NS, c * NS, (int)c0, acc);
+        bulk_commit();
       }
     }
   }
+  if (issuer) bulk_wait0();
 }
 
+// ---------------------------------------------------------------------------
+// host tables
+// ---------------------------------------------------------------------------
 bool burgers_supported(int nq, int ns) { return ns == bz::NS && nq > 0; }
 
-void burgers_tables(int nq, const double* W, const double* B, const double* D, double* out) {
-  // out = [T1 fragments (KS1*NT1*32) | R2 fragments (KS2*NT2*32)]
+int burgers_tables(int nq, const double* W, const double* B, const double* D, double* out) {
+  // out = [S fragments | R2 fragments | Dn]
   using namespace bz;
   const int Q = nq;
   auto Bv = [&](int q, int j) { return B[(size_t)q * NS + j]; };
@@ -404,31 +351,83 @@ void burgers_tables(int nq, const double* W, const double* B, const double* D, d
     *j = 4 * bz_J(ub) + 2 * h + col / 4;
     *k = 4 * bz_K(ub) + col % 4;
   };
-  // T[n][a][j][k] (symmetric in j,k)
-  static thread_local double T[NS][3][NS][NS];
-  for (int n = 0; n < NS; ++n)
-    for (int a = 0; a < 3; ++a)
-      for (int j = 0; j < NS; ++j)
-        for (int k = j; k < NS; ++k) {
+  // ---- orthonormal basis Psi of span{D_a[:, n]} (pivoted modified Gram-Schmidt)
+  std::vector<std::vector<double>> res(3 * NS, std::vector<double>(Q));
+  double maxn = 0.0;
+  for (int a = 0; a < 3; ++a)
+    for (int n = 0; n < NS; ++n) {
+      double s = 0.0;
+      for (int q = 0; q < Q; ++q) {
+        res[a * NS + n][q] = Dv(a, q, n);
+        s += Dv(a, q, n) * Dv(a, q, n);
+      }
+      maxn = std::max(maxn, std::sqrt(s));
+    }
+  std::vector<std::vector<double>> psi;
+  for (;;) {
+    int p = -1;
+    double best = 0.0;
+    for (int i = 0; i < 3 * NS; ++i) {
+      double s = 0.0;
+      for (int q = 0; q < Q; ++q) s += res[i][q] * res[i][q];
+      if (s > best) best = s, p = i;
+    }
+    if (p < 0 || std::sqrt(best) <= 1e-10 * maxn) break;
+    if ((int)psi.size() == RMAX) return -1;
+    std::vector<double> v = res[p];
+    for (int pass = 0; pass < 2; ++pass)
+      for (const auto& b : psi) {
+        double dot = 0.0;
+        for (int q = 0; q < Q; ++q) dot += b[q] * v[q];
+        for (int q = 0; q < Q; ++q) v[q] -= dot * b[q];
+      }
+    double nv = 0.0;
+    for (int q = 0; q < Q; ++q) nv += v[q] * v[q];
+    nv = std::sqrt(nv);
+    for (int q = 0; q < Q; ++q) v[q] /= nv;
+    for (auto& r : res) {
+      double dot = 0.0;
+      for (int q = 0; q < Q; ++q) dot += v[q] * r[q];
+      for (int q = 0; q < Q; ++q) r[q] -= dot * v[q];
+    }
+    psi.push_back(v);
+  }
+  const int rank = (int)psi.size();
+  // Dn_a = Psi^T D_a; check D_a == Psi Dn_a
+  double* Dn = out + S_DBL + R2_DBL;
+  for (int i = 0; i < DN_DBL; ++i) Dn[i] = 0.0;
+  double err = 0.0, amax = 0.0;
+  for (int a = 0; a < 3; ++a)
+    for (int n = 0; n < NS; ++n) {
+      for (int m = 0; m < rank; ++m) {
+        double s = 0.0;
+        for (int q = 0; q < Q; ++q) s += psi[m][q] * Dv(a, q, n);
+        Dn[(a * RMAX + m) * NS + n] = s;
+      }
+      for (int q = 0; q < Q; ++q) {
+        double s = 0.0;
+        for (int m = 0; m < rank; ++m) s += psi[m][q] * Dn[(a * RMAX + m) * NS + n];
+        err = std::max(err, std::fabs(s - Dv(a, q, n)));
+        amax = std::max(amax, std::fabs(Dv(a, q, n)));
+      }
+    }
+  if (err > 1e-12 * std::max(amax, 1.0)) return -1;
+  // S fragments: b = S[m = 4ks + t][col g]
+  for (int ub = 0; ub < NBU; ++ub)
+    for (int ks = 0; ks < KS1; ++ks)
+      for (int h = 0; h < 2; ++h)
+        for (int lane = 0; lane < 32; ++lane) {
+          const int g = lane >> 2, t = lane & 3, m = ks * 4 + t;
+          int j, k;
+          jk_of(ub, h, g, &j, &k);
           double s = 0.0;
-          for (int q = 0; q < Q; ++q) s += W[q] * Dv(a, q, n) * Bv(q, j) * Bv(q, k);
-          T[n][a][j][k] = T[n][a][k][j] = s;
+          if (m < rank)
+            for (int q = 0; q < Q; ++q) s += W[q] * psi[m][q] * Bv(q, j) * Bv(q, k);
+          out[((ub * KS1 + ks) * 2 + h) * 32 + lane] = s;
         }
-  for (int ks = 0; ks < KS1; ++ks)
-    for (int a = 0; a < 3; ++a)
-      for (int ub = 0; ub < NBU; ++ub)
-        for (int h = 0; h < 2; ++h)
-          for (int lane = 0; lane < 32; ++lane) {
-            const int g = lane >> 2, t = lane & 3;
-            const int n = ks * 4 + t;
-            int j, k;
-            jk_of(ub, h, g, &j, &k);
-            out[((size_t)ks * NT1 + (a * NBU + ub) * 2 + h) * 32 + lane] =
-                n < NS ? T[n][a][j][k] : 0.0;
-          }
   // R2[alpha][j][k]
-  static thread_local double R2[KS2 * 4][NS][NS];
-  for (int al = 0; al < KS2 * 4; ++al)
+  std::vector<double> R2((size_t)KS2 * 4 * NS * NS, 0.0);
+  for (int al = 0; al < 67; ++al)
     for (int j = 0; j < NS; ++j)
       for (int k = 0; k < NS; ++k) {
         double s = 0.0;
@@ -443,46 +442,55 @@ void burgers_tables(int nq, const double* W, const double* B, const double* D, d
             const int b = sI < 3 ? sI : (sI == 3 ? 1 : 2);
             v = Dv(a, q, j) * Dv(b, q, k);
             if (a != b) v += Dv(b, q, j) * Dv(a, q, k);
-          } else if (al == 66) {
+          } else {
             v = Bv(q, j) * Bv(q, k);
           }
           s += W[q] * v;
         }
-        R2[al][j][k] = s;
+        R2[((size_t)al * NS + j) * NS + k] = s;
       }
-  // [pass][ks][slot][32]: warp w's slots of pass p start at bz_slot_base(w, p)
-  double* r2 = out + T1_DBL;
-  for (int p = 0; p < 2; ++p) {
-    const int slots = p ? SLOTS1 : SLOTS0;
-    double* base = r2 + (p ? R2_OFF1 : 0);
-    for (int w = 0; w < WARPS; ++w) {
-      const int ub = kWblk[w][p];
-      if (ub < 0) continue;
-      const bool off = bz_J(ub) != bz_K(ub);
-      const int s0 = bz_slot_base(w, p);
+  double* r2 = out + S_DBL;
+  for (int ub = 0; ub < NBU; ++ub) {
+    const bool off = bz_J(ub) != bz_K(ub);
+    for (int ks = 0; ks < KS2; ++ks)
       for (int h = 0; h < 2; ++h)
-        for (int ks = 0; ks < KS2; ++ks)
-          for (int lane = 0; lane < 32; ++lane) {
-            const int g = lane >> 2, t = lane & 3;
-            int j, k;
-            jk_of(ub, h, g, &j, &k);
-            const int al = ks * 4 + t;
-            // direct tile: C[j][k]
-            base[((size_t)ks * slots + s0 + h) * 32 + lane] = R2[al][j][k];
-            // mirror tile: the lane that writes position (k, j) needs C[k][j]
-            if (off) base[((size_t)ks * slots + s0 + 2 + h) * 32 + lane] = R2[al][k][j];
-          }
-    }
+        for (int lane = 0; lane < 32; ++lane) {
+          const int g = lane >> 2, t = lane & 3, al = ks * 4 + t;
+          int j, k;
+          jk_of(ub, h, g, &j, &k);
+          // direct tile: C[j][k]; mirror tile: the lane writing (k, j) needs C[k][j]
+          r2[((ub * KS2 + ks) * 4 + h) * 32 + lane] = R2[((size_t)al * NS + j) * NS + k];
+          r2[((ub * KS2 + ks) * 4 + 2 + h) * 32 + lane] =
+              off ? R2[((size_t)al * NS + k) * NS + j] : 0.0;
+        }
   }
+  return rank;
 }
 
-size_t burgers_table_doubles() { return bz::T1_DBL + bz::R2_DBL; }
+size_t burgers_table_doubles() { return bz::S_DBL + bz::R2_DBL + bz::DN_DBL; }
+
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+}  // namespace
 
 cudaError_t launch_burgers(int ns, long E, const double* coords, const double* coef,
                            const double* tab, double nu, double dt, double* A, int acc,
                            cudaStream_t s) {
   if (ns != bz::NS) return cudaErrorInvalidValue;
   if (E <= 0) return cudaSuccess;
+  if (E > 0x7fffffffL) return cudaErrorInvalidValue;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(burgers_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -490,9 +498,21 @@ cudaError_t launch_burgers(int ns, long E, const double* coords, const double* c
     if (e != cudaSuccess) return e;
     configured = true;
   }
+  auto encode = encode_fn();
+  if (!encode) return cudaErrorNotSupported;
+  // A_e as a 3D tensor [E][60 rows][60 cols]; box = one (c,d) block of 16 cells
+  CUtensorMap map;
+  const cuuint64_t dims[3] = {(cuuint64_t)bz::N, (cuuint64_t)bz::N, (cuuint64_t)E};
+  const cuuint64_t strides[2] = {bz::N * sizeof(double), (cuuint64_t)bz::N * bz::N * sizeof(double)};
+  const cuuint32_t box[3] = {bz::NS, bz::NS, bz::CELLS};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  if (encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, A, dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
   const long ntiles = (E + bz::CELLS - 1) / bz::CELLS;
   const int grid = (int)(ntiles < kNumSMs ? ntiles : kNumSMs);
-  burgers_kernel<<<grid, bz::THREADS, bz::SMEM, s>>>(E, coords, coef, tab, nu, dt, A, acc);
+  burgers_kernel<<<grid, bz::THREADS, bz::SMEM, s>>>(map, E, coords, coef, tab, nu, dt, acc);
   return cudaGetLastError();
 }
 

@@ -373,9 +373,17 @@ int femgpu_form_create(const femgpu_form_desc* d, femgpu_form** out) {
         f->route = ROUTE_BURGERS;
         f->schedule = FEMGPU_SCHED_TENSOR;
         host.assign(femgpu::burgers_table_doubles(), 0.0);
-        femgpu::burgers_tables(f->nq, f->W.data(), f->B.data(), f->D.data(), host.data());
-        // GEMM-1: 3 c x 20 n x 630 (a,p); GEMM-2: 67 x 400; epilogue 3 x 210 x 3 x 4
-        f->flops_per_cell = 2.0 * 3 * 20 * 630 + 2.0 * 67 * 400 + 3.0 * 210 * 3 * 4 + 60 * 7 + 60;
+        {
+          const int r = femgpu::burgers_tables(f->nq, f->W.data(), f->B.data(), f->D.data(),
+                                               host.data());
+          if (r < 0)
+            throw Error(FEMGPU_ERR_UNSUPPORTED,
+                        "Burgers kernel: derivative tables do not span a space of rank <= 12");
+          // g^{cd}: 3c x 3a x r x 20 + 9 x r x 3; GEMM-1: 9 (c,d) x r x 210 (j<=k);
+          // GEMM-2: 67 x 400; geometry + GEMM-2 A
+          f->flops_per_cell = 2.0 * 9 * r * 20 + 2.0 * 9 * r * 3 + 2.0 * 9 * r * 210 +
+                              2.0 * 67 * 400 + 60 * 7 + 60;
+        }
         f->kernel_name = "burgers_kernel";
     }
     if (!host.empty()) {

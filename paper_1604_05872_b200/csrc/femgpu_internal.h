@@ -35,7 +35,8 @@ cudaError_t launch_pair(int kind, int nq, int ns, long E, const double* coords,
 // Burgers tensor schedule (see burgers.cu).
 bool burgers_supported(int nq, int ns);
 size_t burgers_table_doubles();
-void burgers_tables(int nq, const double* W, const double* B, const double* D, double* out);
+// Returns the derivative-space rank used by GEMM-1, or -1 if unsupported.
+int burgers_tables(int nq, const double* W, const double* B, const double* D, double* out);
 cudaError_t launch_burgers(int ns, long E, const double* coords, const double* coef,
                            const double* tab, double nu, double dt, double* A, int acc,
                            cudaStream_t s);
