@@ -53,22 +53,32 @@ constexpr int N = 60;
 constexpr int NBU = 15;            // upper 4x4 blocks (J <= K) of the 20x20 (j,k) plane
 constexpr int KS1 = 3;             // GEMM-1 k4 steps over the derivative space
 constexpr int RMAX = 4 * KS1;      // largest supported derivative-space rank
+constexpr int DNR = 16;            // Dn rows held in smem (two n8 tiles, zero past rank)
 constexpr int KS2 = 18;            // GEMM-2 k4 steps: 60 (n,a) + 6 (G) + 1 (mass) + pad
 constexpr int CELLS = 16;
 constexpr int WARPS = 16;
 constexpr int THREADS = 32 * WARPS;
-constexpr int ISSUER = WARPS - 1;  // warp without a block: TMA stores
+constexpr int CWARPS = 15;         // compute warps, one upper block each
+constexpr int CTHREADS = 32 * CWARPS;
+constexpr int PRODUCER = 15;       // warp 15: inputs, geometry, GEMM A fragments
+constexpr int ISSUER = 14;         // lane 0 of warp 14 issues the slab stores
 constexpr int NSLAB = 3;
 constexpr int SLAB_DBL = CELLS * NS * NS;     // one (c,d) block of 16 cells
 constexpr int S_DBL = NBU * KS1 * 2 * 32;     // GEMM-1 B fragments
 constexpr int R2_DBL = NBU * KS2 * 4 * 32;    // GEMM-2 B fragments
-constexpr int DN_DBL = 3 * RMAX * NS;         // Dn_a (r x 20), zero rows past r
+constexpr int DN_DBL = 3 * DNR * NS;          // Dn_a (r x 20), zero rows past r
 constexpr int A1_DBL = 9 * KS1 * 64;          // g^{cd} fragments
 constexpr int A2_DBL = KS2 * 64;              // GEMM-2 A fragments
-constexpr int IN_DBL = CELLS * (12 + 3 * NS); // coords | u (cp.async target)
+constexpr int COORD_DBL = CELLS * 12;
+constexpr int IN_DBL = CELLS * (12 + 3 * NS); // coords | u (bulk-copy target)
 constexpr int CELLD = 10;                     // K(9), adet
 constexpr size_t SMEM =
-    sizeof(double) * (size_t)(NSLAB * SLAB_DBL + DN_DBL + A1_DBL + A2_DBL + IN_DBL + CELLS * CELLD);
+    sizeof(double) * (size_t)(NSLAB * SLAB_DBL + DN_DBL + 2 * A1_DBL + 2 * A2_DBL + IN_DBL +
+                              CELLS * CELLD) + 16;
+// named barriers (0 = __syncthreads)
+constexpr int BAR_CD = 1;          // compute warps, once per (c,d) block
+constexpr int BAR_FULL = 2;        // + buffer: producer -> compute
+constexpr int BAR_EMPTY = 4;       // + buffer: compute -> producer
 }  // namespace bz
 
 // Upper block u (row-major over J <= K) -> (J, K).
@@ -122,6 +132,13 @@ __device__ __forceinline__ void bulk_wait_read1() {
   asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
 }
 
+__device__ __forceinline__ void nbar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void nbar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+
 __global__ void __launch_bounds__(bz::THREADS, 1)
     burgers_kernel(const __grid_constant__ CUtensorMap amap, long E,
                    const double* __restrict__ coords, const double* __restrict__ u,
@@ -129,91 +146,118 @@ __global__ void __launch_bounds__(bz::THREADS, 1)
   using namespace bz;
   extern __shared__ __align__(1024) double smem[];
   double* sSlab = smem;                    // [NSLAB][CELLS][20][20]  (TMA box layout)
-  double* sDn = sSlab + NSLAB * SLAB_DBL;  // [3][RMAX][20]
-  double* sA1 = sDn + DN_DBL;              // [9][KS1][32][2]
-  double* sA2 = sA1 + A1_DBL;              // [KS2][32][2]
-  double* sIn = sA2 + A2_DBL;              // [CELLS][12] | [CELLS][60]
+  double* sDn = sSlab + NSLAB * SLAB_DBL;  // [3][DNR][20]
+  double* sA1 = sDn + DN_DBL;              // [2][9][KS1][32][2]
+  double* sA2 = sA1 + 2 * A1_DBL;          // [2][KS2][32][2]
+  double* sIn = sA2 + 2 * A2_DBL;          // [CELLS][12] | [CELLS][60]
   double* sCell = sIn + IN_DBL;            // [CELLS][10]
+  uint64_t* inBar = reinterpret_cast<uint64_t*>(sCell + CELLS * CELLD);
   const double* gS = tab;                  // [ub][KS1][2][32]
   const double* gR2 = tab + S_DBL;         // [ub][KS2][4][32]
-  const double* gDn = gR2 + R2_DBL;        // [3][RMAX][20]
+  const double* gDn = gR2 + R2_DBL;        // [3][DNR][20]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int ub = c_wblk[warp];
-  const int J = ub >= 0 ? bz_J(ub) : 0, K = ub >= 0 ? bz_K(ub) : 0;
-  const bool mirror = J != K;
-  const bool issuer = warp == ISSUER && lane == 0;
-  const int hs = g & 1;  // odd-g lanes write the other half first (bank spread)
+  const long ntiles = (E + CELLS - 1) / CELLS;
+  const long my_tiles =
+      (long)blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
 
   for (int i = tid; i < DN_DBL; i += THREADS) sDn[i] = gDn[i];
-  // GEMM-1 B fragments of this warp's block: registers for the whole kernel
-  double sb[KS1][2];
-#pragma unroll
-  for (int ks = 0; ks < KS1; ++ks)
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-      sb[ks][h] = ub >= 0 ? gS[((ub * KS1 + ks) * 2 + h) * 32 + lane] : 0.0;
+  if (tid == 0) {
+    mbar_init(inBar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
 
-  const long ntiles = (E + CELLS - 1) / CELLS;
-  auto prefetch = [&](long tile) {
-    const long c0 = tile * CELLS;
-    const int nt = (int)min((long)CELLS, E - c0);
-    for (int i = tid; i < nt * 12; i += THREADS) cp_async8b(&sIn[i], coords + c0 * 12 + i);
-    for (int i = tid; i < nt * 3 * NS; i += THREADS)
-      cp_async8b(&sIn[CELLS * 12 + i], u + c0 * 3 * NS + i);
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-  };
-  if ((long)blockIdx.x < ntiles) prefetch(blockIdx.x);
-
-  long gi = 0;  // running (c,d) block counter of this CTA: slab gi % NSLAB
-  for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const long c0 = tile * CELLS;
-    const int nt = (int)min((long)CELLS, E - c0);
-    asm volatile("cp.async.wait_all;\n" ::: "memory");
-    __syncthreads();  // inputs landed; previous tile's readers of sA1/sA2 done
-    if (tid < CELLS) {
-      double x[12];
+  if (warp == PRODUCER) {
+    // ===================== producer: inputs -> A fragments =====================
+    auto load = [&](long tile) {  // one bulk copy each for coords and u
+      if (lane == 0) {
+        const long c0 = tile * CELLS;
+        const int nt = (int)min((long)CELLS, E - c0);
+        mbar_expect_tx(inBar, nt * (12 + 3 * NS) * 8);
+        bulk_g2s(sIn, coords + c0 * 12, nt * 12 * 8, inBar);
+        bulk_g2s(sIn + COORD_DBL, u + c0 * 3 * NS, nt * 3 * NS * 8, inBar);
+      }
+    };
+    if (my_tiles > 0) load(blockIdx.x);
+    for (long it = 0; it < my_tiles; ++it) {
+      const long tile = blockIdx.x + it * gridDim.x;
+      const int nt = (int)min((long)CELLS, E - tile * CELLS);
+      const int b = (int)(it & 1);
+      double* A1 = sA1 + b * A1_DBL;
+      double* A2 = sA2 + b * A2_DBL;
+      mbar_wait(inBar, (uint32_t)(it & 1));
+      if (lane < CELLS) {
+        double x[12];
 #pragma unroll
-      for (int r = 0; r < 12; ++r)  // cells past the end: reference tet (never stored)
-        x[r] = tid < nt ? sIn[tid * 12 + r] : ((r == 3 || r == 7 || r == 11) ? 1.0 : 0.0);
-      const Geo geo = cell_geometry(x);
-      double* cd = sCell + tid * CELLD;
+        for (int r = 0; r < 12; ++r)  // cells past the end: reference tet (never stored)
+          x[r] = lane < nt ? sIn[lane * 12 + r] : ((r == 3 || r == 7 || r == 11) ? 1.0 : 0.0);
+        const Geo geo = cell_geometry(x);
+        double* cd = sCell + lane * CELLD;
 #pragma unroll
-      for (int a = 0; a < 3; ++a)
+        for (int a = 0; a < 3; ++a)
 #pragma unroll
-        for (int b = 0; b < 3; ++b) cd[a * 3 + b] = geo.K[a][b];
-      cd[9] = geo.adet;
-    }
-    __syncthreads();
-    // ---- GEMM-1 A: g^{cd}_m = |det| sum_a K_ad (Dn_a u_c)_m; a[v] = A[g+8v][t] ----
-    for (int i = tid; i < CELLS * 3 * RMAX; i += THREADS) {
-      const int cell = i / (3 * RMAX), c = (i / RMAX) % 3, m = i % RMAX;
-      double gu[3] = {0.0, 0.0, 0.0};
-      if (cell < nt) {
-        const double* uc = sIn + CELLS * 12 + cell * 3 * NS + c * NS;
-#pragma unroll 4
-        for (int n = 0; n < NS; ++n) {
-          const double un = uc[n];
+          for (int bb = 0; bb < 3; ++bb) cd[a * 3 + bb] = geo.K[a][bb];
+        cd[9] = lane < nt ? geo.adet : 0.0;  // zero rows for cells past the end
+      }
+      if (it >= 2) nbar_sync(BAR_EMPTY + b, THREADS);  // compute warps done with buffer b
+      __syncwarp();
+      // ---- GEMM-1 A: Gu_a = u_c Dn_a^T on the tensor cores (rows = cells,
+      //      columns = m in two n8 tiles), then g^{cd}_m = |det| sum_a K_ad Gu_a ----
+      const double* uin = sIn + COORD_DBL;
+#pragma unroll 1
+      for (int c = 0; c < 3; ++c) {
+        double gu[3][2][4];
 #pragma unroll
-          for (int a = 0; a < 3; ++a) gu[a] = fma(sDn[(a * RMAX + m) * NS + n], un, gu[a]);
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int tt = 0; tt < 2; ++tt)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) gu[a][tt][v] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < NS / 4; ++ks) {
+          const int n = ks * 4 + t;
+          const double a0 = uin[g * 3 * NS + c * NS + n];
+          const double a1 = uin[(g + 8) * 3 * NS + c * NS + n];
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int tt = 0; tt < 2; ++tt)
+              dmma16x8x4(gu[a][tt], a0, a1, sDn[(a * DNR + 8 * tt + g) * NS + n]);
+        }
+        // gu[a][tt][v] = Gu_a[cell g + 8(v>>1)][m = 8tt + 2t + (v&1)]
+#pragma unroll
+        for (int vh = 0; vh < 2; ++vh) {
+          const int cell = g + 8 * vh;
+          const double* cd = sCell + cell * CELLD;
+          double Kd[3][3];
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int d = 0; d < 3; ++d) Kd[a][d] = cd[9] * cd[a * 3 + d];
+#pragma unroll
+          for (int tt = 0; tt < 2; ++tt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int m = 8 * tt + 2 * t + e;
+              if (m < RMAX) {
+                const int v = 2 * vh + e;
+#pragma unroll
+                for (int d = 0; d < 3; ++d)
+                  A1[(((c * 3 + d) * KS1 + (m >> 2)) * 32 + 4 * (cell & 7) + (m & 3)) * 2 + vh] =
+                      Kd[0][d] * gu[0][tt][v] + Kd[1][d] * gu[1][tt][v] + Kd[2][d] * gu[2][tt][v];
+              }
+            }
         }
       }
-      const double* cd = sCell + cell * CELLD;
-      const int ks = m >> 2, ln = 4 * (cell & 7) + (m & 3), v = cell >> 3;
-#pragma unroll
-      for (int d = 0; d < 3; ++d)
-        sA1[(((c * 3 + d) * KS1 + ks) * 32 + ln) * 2 + v] =
-            cd[9] * (cd[0 * 3 + d] * gu[0] + cd[1 * 3 + d] * gu[1] + cd[2 * 3 + d] * gu[2]);
-    }
-    // ---- GEMM-2 A fragments ----
-    for (int i = tid; i < KS2 * 64; i += THREADS) {
-      const int ks = i / 64, ln = (i % 64) / 2, v = i % 2;
-      const int cell = (ln >> 2) + 8 * v, al = ks * 4 + (ln & 3);
-      const double* cd = sCell + cell * CELLD;
-      const double* uc = sIn + CELLS * 12 + cell * 3 * NS;
-      double val = 0.0;
-      if (cell < nt) {
+      // ---- GEMM-2 A fragments: lane -> (cell, alpha) pairs ----
+      for (int i = lane; i < KS2 * 64; i += 32) {
+        const int ks = i >> 6, ln = (i >> 1) & 31, v = i & 1;
+        const int cell = (ln >> 2) + 8 * v, al = ks * 4 + (ln & 3);
+        const double* cd = sCell + cell * CELLD;
+        const double* uc = uin + cell * 3 * NS;
+        double val = 0.0;
         if (al < 60) {
           const int n = al / 3, a = al % 3;  // beta_{n,a} = sum_b u_{b,n} K_ab
           val = cd[9] * (uc[n] * cd[a * 3 + 0] + uc[NS + n] * cd[a * 3 + 1] +
@@ -221,18 +265,55 @@ __global__ void __launch_bounds__(bz::THREADS, 1)
         } else if (al < 66) {
           const int s = al - 60;  // (0,0),(1,1),(2,2),(0,1),(0,2),(1,2)
           const int a = s < 3 ? s : (s == 5 ? 1 : 0);
-          const int b = s < 3 ? s : (s == 3 ? 1 : 2);
+          const int bb = s < 3 ? s : (s == 3 ? 1 : 2);
           val = cd[9] * nu *
-                (cd[a * 3 + 0] * cd[b * 3 + 0] + cd[a * 3 + 1] * cd[b * 3 + 1] +
-                 cd[a * 3 + 2] * cd[b * 3 + 2]);
+                (cd[a * 3 + 0] * cd[bb * 3 + 0] + cd[a * 3 + 1] * cd[bb * 3 + 1] +
+                 cd[a * 3 + 2] * cd[bb * 3 + 2]);
         } else if (al == 66) {
           val = cd[9] / dt;
         }
+        A2[i] = val;
       }
-      sA2[i] = val;
+      __syncwarp();
+      // sIn fully consumed (reads retired into registers): refill with the next tile
+      if (it + 1 < my_tiles) {
+        fence_proxy_async();
+        load(tile + gridDim.x);
+      }
+      nbar_arrive(BAR_FULL + b, THREADS);
     }
-    __syncthreads();
-    if (tile + gridDim.x < ntiles) prefetch(tile + gridDim.x);
+    return;
+  }
+
+  // ======================= compute warps: one upper block each =================
+  const int ub = c_wblk[warp];
+  const int J = bz_J(ub), K = bz_K(ub);
+  const bool mirror = J != K;
+  const bool issuer = warp == ISSUER && lane == 0;
+  const int hs = g & 1;  // odd-g lanes write the other half first (bank spread)
+  // GEMM-1 B fragments of this warp's block: registers for the whole kernel
+  double sb[KS1][2];
+#pragma unroll
+  for (int ks = 0; ks < KS1; ++ks)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) sb[ks][h] = gS[((ub * KS1 + ks) * 2 + h) * 32 + lane];
+  const double* r2 = gR2 + (size_t)ub * KS2 * 4 * 32 + lane;
+
+  long gi = 0;  // running (c,d) block counter of this CTA: slab gi % NSLAB
+  for (long it = 0; it < my_tiles; ++it) {
+    const long c0 = (blockIdx.x + it * gridDim.x) * CELLS;
+    const int b = (int)(it & 1);
+    const double* A1 = sA1 + b * A1_DBL;
+    const double* A2 = sA2 + b * A2_DBL;
+    // first GEMM-2 B chunk before waiting for the producer (L2 latency)
+    constexpr int CH = 3;  // k4 steps per register chunk (double-buffered)
+    double bq[2][CH][4];
+#pragma unroll
+    for (int kk = 0; kk < CH; ++kk)
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+        bq[0][kk][x] = (x < 2 || mirror) ? ldg_nc(r2 + (kk * 4 + x) * 32) : 0.0;
+    nbar_sync(BAR_FULL + b, THREADS);
 
     // ---- GEMM-2: C direct (tiles 0,1) and mirror (2,3); B from L2 ----------
     double cdir[2][4], cmir[2][4];
@@ -240,37 +321,36 @@ __global__ void __launch_bounds__(bz::THREADS, 1)
     for (int h = 0; h < 2; ++h)
 #pragma unroll
       for (int v = 0; v < 4; ++v) cdir[h][v] = cmir[h][v] = 0.0;
-    if (ub >= 0) {
-      const double* r2 = gR2 + (size_t)ub * KS2 * 4 * 32 + lane;
-      constexpr int CH = 3;  // k4 steps per register chunk (double-buffered)
-      double bq[2][CH][4];
 #pragma unroll
-      for (int kk = 0; kk < CH; ++kk)
+    for (int ch = 0; ch < KS2 / CH; ++ch) {
+      const int cur = ch & 1;
+      if (ch + 1 < KS2 / CH) {
 #pragma unroll
-        for (int x = 0; x < 4; ++x)
-          bq[0][kk][x] = (x < 2 || mirror) ? ldg_nc(r2 + (kk * 4 + x) * 32) : 0.0;
+        for (int kk = 0; kk < CH; ++kk)
 #pragma unroll
-      for (int ch = 0; ch < KS2 / CH; ++ch) {
-        const int cur = ch & 1;
-        if (ch + 1 < KS2 / CH) {
+          for (int x = 0; x < 4; ++x)
+            bq[cur ^ 1][kk][x] =
+                (x < 2 || mirror) ? ldg_nc(r2 + (((ch + 1) * CH + kk) * 4 + x) * 32) : 0.0;
+      }
 #pragma unroll
-          for (int kk = 0; kk < CH; ++kk)
-#pragma unroll
-            for (int x = 0; x < 4; ++x)
-              bq[cur ^ 1][kk][x] =
-                  (x < 2 || mirror) ? ldg_nc(r2 + (((ch + 1) * CH + kk) * 4 + x) * 32) : 0.0;
-        }
-#pragma unroll
-        for (int kk = 0; kk < CH; ++kk) {
-          const double2 af = reinterpret_cast<const double2*>(sA2)[(ch * CH + kk) * 32 + lane];
-          dmma16x8x4(cdir[0], af.x, af.y, bq[cur][kk][0]);
-          dmma16x8x4(cdir[1], af.x, af.y, bq[cur][kk][1]);
-          if (mirror) {
-            dmma16x8x4(cmir[0], af.x, af.y, bq[cur][kk][2]);
-            dmma16x8x4(cmir[1], af.x, af.y, bq[cur][kk][3]);
-          }
+      for (int kk = 0; kk < CH; ++kk) {
+        const double2 af = reinterpret_cast<const double2*>(A2)[(ch * CH + kk) * 32 + lane];
+        dmma16x8x4(cdir[0], af.x, af.y, bq[cur][kk][0]);
+        dmma16x8x4(cdir[1], af.x, af.y, bq[cur][kk][1]);
+        if (mirror) {
+          dmma16x8x4(cmir[0], af.x, af.y, bq[cur][kk][2]);
+          dmma16x8x4(cmir[1], af.x, af.y, bq[cur][kk][3]);
         }
       }
+    }
+    // odd-g lanes handle half 1 first: swap C once per tile
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const double d0 = cdir[0][v], d1 = cdir[1][v], m0 = cmir[0][v], m1 = cmir[1][v];
+      cdir[0][v] = hs ? d1 : d0;
+      cdir[1][v] = hs ? d0 : d1;
+      cmir[0][v] = hs ? m1 : m0;
+      cmir[1][v] = hs ? m0 : m1;
     }
 
     // ---- the nine (c,d) blocks: GEMM-1, + C on the diagonal, slab, TMA ----
@@ -278,59 +358,58 @@ __global__ void __launch_bounds__(bz::THREADS, 1)
     for (int cdi = 0; cdi < 9; ++cdi, ++gi) {
       const int c = cdi / 3, d = cdi % 3;
       double* slab = sSlab + (gi % NSLAB) * SLAB_DBL;
-      if (ub >= 0) {
-        double m[2][4];
+      double m[2][4];
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
+      for (int h = 0; h < 2; ++h)
 #pragma unroll
-          for (int v = 0; v < 4; ++v) m[h][v] = 0.0;
+        for (int v = 0; v < 4; ++v) m[h][v] = 0.0;
 #pragma unroll
-        for (int ks = 0; ks < KS1; ++ks) {
-          const double2 af = reinterpret_cast<const double2*>(sA1)[(cdi * KS1 + ks) * 32 + lane];
-          dmma16x8x4(m[0], af.x, af.y, sb[ks][0]);
-          dmma16x8x4(m[1], af.x, af.y, sb[ks][1]);
+      for (int ks = 0; ks < KS1; ++ks) {
+        const double2 af = reinterpret_cast<const double2*>(A1)[(cdi * KS1 + ks) * 32 + lane];
+        dmma16x8x4(m[0], af.x, af.y, sb[ks][0]);
+        dmma16x8x4(m[1], af.x, af.y, sb[ks][1]);
+      }
+      const double dg = c == d ? 1.0 : 0.0;
+      // C fragment c[v] = C[cell g + 8(v>>1)][col 2t + (v&1)];
+      // col -> (j, k) = (4J + 2h + t/2, 4K + 2(t&1) + e)
+#pragma unroll
+      for (int hi = 0; hi < 2; ++hi) {
+        const int h = hi ^ hs;
+        double dv[4], rv[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const double mv = hs ? m[hi ^ 1][v] : m[hi][v];
+          dv[v] = fma(dg, cdir[hi][v], mv);
+          rv[v] = fma(dg, cmir[hi][v], mv);
         }
-        const double dg = c == d ? 1.0 : 0.0;
-        // C fragment c[v] = C[cell g + 8(v>>1)][col 2t + (v&1)];
-        // col -> (j, k) = (4J + 2h + t/2, 4K + 2(t&1) + e)
+        const int j = 4 * J + 2 * h + (t >> 1);
+        const int k = 4 * K + 2 * (t & 1);
 #pragma unroll
-        for (int hi = 0; hi < 2; ++hi) {
-          const int h = hi ^ hs;
-          double dv[4], rv[4];
-#pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            const double mv = hs ? m[hi ^ 1][v] : m[hi][v];
-            dv[v] = fma(dg, hs ? cdir[hi ^ 1][v] : cdir[hi][v], mv);
-            rv[v] = fma(dg, hs ? cmir[hi ^ 1][v] : cmir[hi][v], mv);
-          }
-          const int j = 4 * J + 2 * h + (t >> 1);
-          const int k = 4 * K + 2 * (t & 1);
-#pragma unroll
-          for (int vh = 0; vh < 2; ++vh) {
-            double* cellp = slab + (g + 8 * vh) * (NS * NS);
-            *reinterpret_cast<double2*>(cellp + j * NS + k) =
-                make_double2(dv[2 * vh], dv[2 * vh + 1]);
-            if (mirror) {
-              // mirror: rows k+e, column j.  Lanes t and t^2 hold columns j, j+1
-              // of rows k, k+1: swap one value so each lane writes 16 bytes.
-              const bool lo = (t >> 1) == 0;
-              const double other =
-                  __shfl_xor_sync(0xffffffffu, lo ? rv[2 * vh + 1] : rv[2 * vh], 2);
-              const int jj0 = 4 * J + 2 * h;
-              *reinterpret_cast<double2*>(cellp + (k + (lo ? 0 : 1)) * NS + jj0) =
-                  lo ? make_double2(rv[2 * vh], other) : make_double2(other, rv[2 * vh + 1]);
-            }
+        for (int vh = 0; vh < 2; ++vh) {
+          double* cellp = slab + (g + 8 * vh) * (NS * NS);
+          *reinterpret_cast<double2*>(cellp + j * NS + k) =
+              make_double2(dv[2 * vh], dv[2 * vh + 1]);
+          if (mirror) {
+            // mirror: rows k+e, column j.  Lanes t and t^2 hold columns j, j+1
+            // of rows k, k+1: swap one value so each lane writes 16 bytes.
+            const bool lo = (t >> 1) == 0;
+            const double other =
+                __shfl_xor_sync(0xffffffffu, lo ? rv[2 * vh + 1] : rv[2 * vh], 2);
+            const int jj0 = 4 * J + 2 * h;
+            *reinterpret_cast<double2*>(cellp + (k + (lo ? 0 : 1)) * NS + jj0) =
+                lo ? make_double2(rv[2 * vh], other) : make_double2(other, rv[2 * vh + 1]);
           }
         }
       }
       fence_proxy_async();  // generic-proxy slab writes -> visible to the TMA unit
       if (issuer) bulk_wait_read1();  // slab of block gi-2 free before anyone writes it next
-      __syncthreads();
+      nbar_sync(BAR_CD, CTHREADS);
       if (issuer) {
         slab_store(&amap, slab, d * NS, c * NS, (int)c0, acc);
         bulk_commit();
       }
     }
+    if (it + 2 < my_tiles) nbar_arrive(BAR_EMPTY + b, THREADS);
   }
   if (issuer) bulk_wait0();
 }
@@ -402,11 +481,11 @@ int burgers_tables(int nq, const double* W, const double* B, const double* D, do
       for (int m = 0; m < rank; ++m) {
         double s = 0.0;
         for (int q = 0; q < Q; ++q) s += psi[m][q] * Dv(a, q, n);
-        Dn[(a * RMAX + m) * NS + n] = s;
+        Dn[(a * DNR + m) * NS + n] = s;
       }
       for (int q = 0; q < Q; ++q) {
         double s = 0.0;
-        for (int m = 0; m < rank; ++m) s += psi[m][q] * Dn[(a * RMAX + m) * NS + n];
+        for (int m = 0; m < rank; ++m) s += psi[m][q] * Dn[(a * DNR + m) * NS + n];
         err = std::max(err, std::fabs(s - Dv(a, q, n)));
         amax = std::max(amax, std::fabs(Dv(a, q, n)));
       }
