@@ -108,6 +108,14 @@ __device__ __forceinline__ double ldg_nc(const double* p) {
   return v;
 }
 
+__device__ __forceinline__ double2 ldg_nc2(const double2* p) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];\n"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(p));
+  return v;
+}
+
 __device__ __forceinline__ void cp_async8b(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
@@ -297,7 +305,7 @@ __global__ void __launch_bounds__(bz::THREADS, 1)
   for (int ks = 0; ks < KS1; ++ks)
 #pragma unroll
     for (int h = 0; h < 2; ++h) sb[ks][h] = gS[((ub * KS1 + ks) * 2 + h) * 32 + lane];
-  const double* r2 = gR2 + (size_t)ub * KS2 * 4 * 32 + lane;
+  const double2* r2 = reinterpret_cast<const double2*>(gR2) + (size_t)ub * KS2 * 2 * 32 + lane;
 
   long gi = 0;  // running (c,d) block counter of this CTA: slab gi % NSLAB
   for (long it = 0; it < my_tiles; ++it) {
@@ -307,12 +315,12 @@ __global__ void __launch_bounds__(bz::THREADS, 1)
     const double* A2 = sA2 + b * A2_DBL;
     // first GEMM-2 B chunk before waiting for the producer (L2 latency)
     constexpr int CH = 3;  // k4 steps per register chunk (double-buffered)
-    double bq[2][CH][4];
+    double2 bq[2][CH][2];
 #pragma unroll
-    for (int kk = 0; kk < CH; ++kk)
-#pragma unroll
-      for (int x = 0; x < 4; ++x)
-        bq[0][kk][x] = (x < 2 || mirror) ? ldg_nc(r2 + (kk * 4 + x) * 32) : 0.0;
+    for (int kk = 0; kk < CH; ++kk) {
+      bq[0][kk][0] = ldg_nc2(r2 + (kk * 2 + 0) * 32);
+      bq[0][kk][1] = mirror ? ldg_nc2(r2 + (kk * 2 + 1) * 32) : make_double2(0.0, 0.0);
+    }
     nbar_sync(BAR_FULL + b, THREADS);
 
     // ---- GEMM-2: C direct (tiles 0,1) and mirror (2,3); B from L2 ----------
@@ -326,20 +334,20 @@ __global__ void __launch_bounds__(bz::THREADS, 1)
       const int cur = ch & 1;
       if (ch + 1 < KS2 / CH) {
 #pragma unroll
-        for (int kk = 0; kk < CH; ++kk)
-#pragma unroll
-          for (int x = 0; x < 4; ++x)
-            bq[cur ^ 1][kk][x] =
-                (x < 2 || mirror) ? ldg_nc(r2 + (((ch + 1) * CH + kk) * 4 + x) * 32) : 0.0;
+        for (int kk = 0; kk < CH; ++kk) {
+          const int ks = (ch + 1) * CH + kk;
+          bq[cur ^ 1][kk][0] = ldg_nc2(r2 + (ks * 2 + 0) * 32);
+          bq[cur ^ 1][kk][1] = mirror ? ldg_nc2(r2 + (ks * 2 + 1) * 32) : make_double2(0.0, 0.0);
+        }
       }
 #pragma unroll
       for (int kk = 0; kk < CH; ++kk) {
         const double2 af = reinterpret_cast<const double2*>(A2)[(ch * CH + kk) * 32 + lane];
-        dmma16x8x4(cdir[0], af.x, af.y, bq[cur][kk][0]);
-        dmma16x8x4(cdir[1], af.x, af.y, bq[cur][kk][1]);
+        dmma16x8x4(cdir[0], af.x, af.y, bq[cur][kk][0].x);
+        dmma16x8x4(cdir[1], af.x, af.y, bq[cur][kk][0].y);
         if (mirror) {
-          dmma16x8x4(cmir[0], af.x, af.y, bq[cur][kk][2]);
-          dmma16x8x4(cmir[1], af.x, af.y, bq[cur][kk][3]);
+          dmma16x8x4(cmir[0], af.x, af.y, bq[cur][kk][1].x);
+          dmma16x8x4(cmir[1], af.x, af.y, bq[cur][kk][1].y);
         }
       }
     }
@@ -369,35 +377,48 @@ __global__ void __launch_bounds__(bz::THREADS, 1)
         dmma16x8x4(m[0], af.x, af.y, sb[ks][0]);
         dmma16x8x4(m[1], af.x, af.y, sb[ks][1]);
       }
-      const double dg = c == d ? 1.0 : 0.0;
+      // odd-g lanes: half 1 first
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const double m0 = m[0][v], m1 = m[1][v];
+        m[0][v] = hs ? m1 : m0;
+        m[1][v] = hs ? m0 : m1;
+      }
+      double r[2][4];  // mirror values
+#pragma unroll
+      for (int hi = 0; hi < 2; ++hi)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) r[hi][v] = m[hi][v];
+      if (c == d) {
+#pragma unroll
+        for (int hi = 0; hi < 2; ++hi)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            r[hi][v] += cmir[hi][v];
+            m[hi][v] += cdir[hi][v];
+          }
+      }
       // C fragment c[v] = C[cell g + 8(v>>1)][col 2t + (v&1)];
       // col -> (j, k) = (4J + 2h + t/2, 4K + 2(t&1) + e)
 #pragma unroll
       for (int hi = 0; hi < 2; ++hi) {
         const int h = hi ^ hs;
-        double dv[4], rv[4];
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const double mv = hs ? m[hi ^ 1][v] : m[hi][v];
-          dv[v] = fma(dg, cdir[hi][v], mv);
-          rv[v] = fma(dg, cmir[hi][v], mv);
-        }
         const int j = 4 * J + 2 * h + (t >> 1);
         const int k = 4 * K + 2 * (t & 1);
 #pragma unroll
         for (int vh = 0; vh < 2; ++vh) {
           double* cellp = slab + (g + 8 * vh) * (NS * NS);
           *reinterpret_cast<double2*>(cellp + j * NS + k) =
-              make_double2(dv[2 * vh], dv[2 * vh + 1]);
+              make_double2(m[hi][2 * vh], m[hi][2 * vh + 1]);
           if (mirror) {
             // mirror: rows k+e, column j.  Lanes t and t^2 hold columns j, j+1
             // of rows k, k+1: swap one value so each lane writes 16 bytes.
             const bool lo = (t >> 1) == 0;
             const double other =
-                __shfl_xor_sync(0xffffffffu, lo ? rv[2 * vh + 1] : rv[2 * vh], 2);
+                __shfl_xor_sync(0xffffffffu, lo ? r[hi][2 * vh + 1] : r[hi][2 * vh], 2);
             const int jj0 = 4 * J + 2 * h;
             *reinterpret_cast<double2*>(cellp + (k + (lo ? 0 : 1)) * NS + jj0) =
-                lo ? make_double2(rv[2 * vh], other) : make_double2(other, rv[2 * vh + 1]);
+                lo ? make_double2(r[hi][2 * vh], other) : make_double2(other, r[hi][2 * vh + 1]);
           }
         }
       }
@@ -538,8 +559,8 @@ int burgers_tables(int nq, const double* W, const double* B, const double* D, do
           int j, k;
           jk_of(ub, h, g, &j, &k);
           // direct tile: C[j][k]; mirror tile: the lane writing (k, j) needs C[k][j]
-          r2[((ub * KS2 + ks) * 4 + h) * 32 + lane] = R2[((size_t)al * NS + j) * NS + k];
-          r2[((ub * KS2 + ks) * 4 + 2 + h) * 32 + lane] =
+          r2[(((ub * KS2 + ks) * 2 + 0) * 32 + lane) * 2 + h] = R2[((size_t)al * NS + j) * NS + k];
+          r2[(((ub * KS2 + ks) * 2 + 1) * 32 + lane) * 2 + h] =
               off ? R2[((size_t)al * NS + k) * NS + j] : 0.0;
         }
   }
