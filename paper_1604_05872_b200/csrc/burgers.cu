@@ -259,28 +259,39 @@ __global__ void __launch_bounds__(bz::THREADS, 1)
             }
         }
       }
-      // ---- GEMM-2 A fragments: lane -> (cell, alpha) pairs ----
-      for (int i = lane; i < KS2 * 64; i += 32) {
-        const int ks = i >> 6, ln = (i >> 1) & 31, v = i & 1;
-        const int cell = (ln >> 2) + 8 * v, al = ks * 4 + (ln & 3);
+      // ---- GEMM-2 A fragments a[v] = A[cell g + 8v][alpha = 4ks + t] ----
+      {
+        const int cell = lane & 15;
         const double* cd = sCell + cell * CELLD;
+        double Kc[9];
+        const double ad = cd[9];
+#pragma unroll
+        for (int i = 0; i < 9; ++i) Kc[i] = cd[i];
         const double* uc = uin + cell * 3 * NS;
-        double val = 0.0;
-        if (al < 60) {
-          const int n = al / 3, a = al % 3;  // beta_{n,a} = sum_b u_{b,n} K_ab
-          val = cd[9] * (uc[n] * cd[a * 3 + 0] + uc[NS + n] * cd[a * 3 + 1] +
-                         uc[2 * NS + n] * cd[a * 3 + 2]);
-        } else if (al < 66) {
-          const int s = al - 60;  // (0,0),(1,1),(2,2),(0,1),(0,2),(1,2)
-          const int a = s < 3 ? s : (s == 5 ? 1 : 0);
-          const int bb = s < 3 ? s : (s == 3 ? 1 : 2);
-          val = cd[9] * nu *
-                (cd[a * 3 + 0] * cd[bb * 3 + 0] + cd[a * 3 + 1] * cd[bb * 3 + 1] +
-                 cd[a * 3 + 2] * cd[bb * 3 + 2]);
-        } else if (al == 66) {
-          val = cd[9] / dt;
+        auto put = [&](int al, double val) {
+          A2[((al >> 2) * 32 + 4 * (cell & 7) + (al & 3)) * 2 + (cell >> 3)] = val;
+        };
+        // beta_{n,a} = |det| sum_b u_{b,n} K_ab at alpha = 3n + a
+#pragma unroll 2
+        for (int n = lane >> 4; n < NS; n += 2) {
+          const double u0 = uc[n], u1 = uc[NS + n], u2 = uc[2 * NS + n];
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+            put(3 * n + a, ad * (Kc[a * 3 + 0] * u0 + Kc[a * 3 + 1] * u1 + Kc[a * 3 + 2] * u2));
         }
-        A2[i] = val;
+        if (lane < 16) {  // nu |det| (K K^T)_s at 60..65, |det|/dt at 66, zero pad
+#pragma unroll
+          for (int s6 = 0; s6 < 6; ++s6) {
+            const int a = s6 < 3 ? s6 : (s6 == 5 ? 1 : 0);
+            const int bb = s6 < 3 ? s6 : (s6 == 3 ? 1 : 2);
+            put(60 + s6, ad * nu *
+                             (Kc[a * 3 + 0] * Kc[bb * 3 + 0] + Kc[a * 3 + 1] * Kc[bb * 3 + 1] +
+                              Kc[a * 3 + 2] * Kc[bb * 3 + 2]));
+          }
+          put(66, ad / dt);
+#pragma unroll
+          for (int al = 67; al < 4 * KS2; ++al) put(al, 0.0);
+        }
       }
       __syncwarp();
       // sIn fully consumed (reads retired into registers): refill with the next tile
