@@ -65,16 +65,20 @@ constexpr int ISSUER = 14;         // lane 0 of warp 14 issues the slab stores
 constexpr int NSLAB = 3;
 constexpr int SLAB_DBL = CELLS * NS * NS;     // one (c,d) block of 16 cells
 constexpr int S_DBL = NBU * KS1 * 2 * 32;     // GEMM-1 B fragments
-constexpr int R2_DBL = NBU * KS2 * 4 * 32;    // GEMM-2 B fragments
+constexpr int R2_DBL = KS2 * 25 * 64;         // GEMM-2 B fragments [ks][pair][32][2]
 constexpr int DN_DBL = 3 * DNR * NS;          // Dn_a (r x 20), zero rows past r
 constexpr int A1_DBL = 9 * KS1 * 64;          // g^{cd} fragments
 constexpr int A2_DBL = KS2 * 64;              // GEMM-2 A fragments
 constexpr int COORD_DBL = CELLS * 12;
 constexpr int IN_DBL = CELLS * (12 + 3 * NS); // coords | u (bulk-copy target)
 constexpr int CELLD = 10;                     // K(9), adet
+constexpr int NPAIR = 25;                     // GEMM-2 B tile pairs: 15 direct + 10 mirror
+constexpr int STAGE_DBL = NPAIR * 64;         // one k4 step of R2
+constexpr int NRING = 8;                      // ring stages (alias slabs 0 and 1)
 constexpr size_t SMEM =
     sizeof(double) * (size_t)(NSLAB * SLAB_DBL + DN_DBL + 2 * A1_DBL + 2 * A2_DBL + IN_DBL +
-                              CELLS * CELLD) + 16;
+                              CELLS * CELLD) + 8 * (1 + 2 * 8);
+static_assert(NRING * STAGE_DBL <= 2 * SLAB_DBL, "R2 ring aliases slabs 0 and 1");
 // named barriers (0 = __syncthreads)
 constexpr int BAR_CD = 1;          // compute warps, once per (c,d) block
 constexpr int BAR_FULL = 2;        // + buffer: producer -> compute
@@ -89,14 +93,18 @@ __host__ __device__ constexpr int bz_K(int u) {
   return u < 5 ? u : u < 9 ? u - 4 : u < 12 ? u - 7 : u < 14 ? u - 9 : 4;
 }
 
+// Off-diagonal upper blocks in order -> 0..9 (their mirror GEMM-2 tile pair).
+__host__ __device__ constexpr int bz_off_index(int u) {
+  return u < 5 ? u - 1 : u < 9 ? u - 2 : u < 12 ? u - 3 : u < 14 ? u - 4 : -1;
+}
+
 // Warp -> upper block.  Sub-partition s runs warps s, s+4, s+8, s+12; the ten
 // off-diagonal blocks (GEMM-2: 72 DMMA/tile) and five diagonal ones (36) are
 // spread so that no sub-partition carries more than 3 off + 1 diagonal.
 __constant__ int c_wblk[bz::WARPS] = {1, 2, 3, 4, 6, 7, 8, 10, 11, 13, 0, 5, 9, 12, 14, -1};
 
 __device__ __forceinline__ void dmma16x8x4(double (&c)[4], double a0, double a1, double b) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 "
+  asm("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 "
       "{%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
       : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
       : "d"(a0), "d"(a1), "d"(b));
@@ -140,12 +148,32 @@ __device__ __forceinline__ void bulk_wait_read1() {
   asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void nbar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
 }
 __device__ __forceinline__ void nbar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory");
 }
+
+#ifdef BZ_TRACE
+// development trace (CTA 0 only): clock64 at pipeline milestones per tile
+__device__ unsigned long long bz_trace[128][16];
+#define BZ_MARK(it, slot, cond) \
+  if (blockIdx.x == 0 && (cond) && (it) < 128) bz_trace[it][slot] = clock64()
+#define BZ_T0() const unsigned long long bz_t0 = clock64()
+#define BZ_ACC(it, slot) \
+  if (blockIdx.x == 0 && (it) < 128) bz_trace[it][slot] += clock64() - bz_t0
+extern "C" int femgpu_debug_trace(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, bz_trace, sizeof(bz_trace));
+}
+#else
+#define BZ_MARK(it, slot, cond)
+#define BZ_T0()
+#define BZ_ACC(it, slot)
+#endif
 
 __global__ void __launch_bounds__(bz::THREADS, 1)
     burgers_kernel(const __grid_constant__ CUtensorMap amap, long E,
@@ -160,8 +188,11 @@ __global__ void __launch_bounds__(bz::THREADS, 1)
   double* sIn = sA2 + 2 * A2_DBL;          // [CELLS][12] | [CELLS][60]
   double* sCell = sIn + IN_DBL;            // [CELLS][10]
   uint64_t* inBar = reinterpret_cast<uint64_t*>(sCell + CELLS * CELLD);
+  uint64_t* rFull = inBar + 1;             // [NRING] R2 stage landed
+  uint64_t* rEmpty = rFull + NRING;        // [NRING] R2 stage consumed by all compute warps
+  double* sRing = sSlab;                   // [NRING][25][32][2]  (aliases slabs 0, 1)
   const double* gS = tab;                  // [ub][KS1][2][32]
-  const double* gR2 = tab + S_DBL;         // [ub][KS2][4][32]
+  const double* gR2 = tab + S_DBL;         // [KS2][25][32][2]
   const double* gDn = gR2 + R2_DBL;        // [3][DNR][20]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -173,6 +204,10 @@ __global__ void __launch_bounds__(bz::THREADS, 1)
   for (int i = tid; i < DN_DBL; i += THREADS) sDn[i] = gDn[i];
   if (tid == 0) {
     mbar_init(inBar, 1);
+    for (int r = 0; r < NRING; ++r) {
+      mbar_init(&rFull[r], 1);
+      mbar_init(&rEmpty[r], CWARPS);
+    }
     fence_mbar_init();
   }
   __syncthreads();
@@ -196,6 +231,7 @@ __global__ void __launch_bounds__(bz::THREADS, 1)
       double* A1 = sA1 + b * A1_DBL;
       double* A2 = sA2 + b * A2_DBL;
       mbar_wait(inBar, (uint32_t)(it & 1));
+      BZ_MARK(it, 0, lane == 0);
       if (lane < CELLS) {
         double x[12];
 #pragma unroll
@@ -210,6 +246,7 @@ __global__ void __launch_bounds__(bz::THREADS, 1)
         cd[9] = lane < nt ? geo.adet : 0.0;  // zero rows for cells past the end
       }
       if (it >= 2) nbar_sync(BAR_EMPTY + b, THREADS);  // compute warps done with buffer b
+      BZ_MARK(it, 1, lane == 0);
       __syncwarp();
       // ---- GEMM-1 A: Gu_a = u_c Dn_a^T on the tensor cores (rows = cells,
       //      columns = m in two n8 tiles), then g^{cd}_m = |det| sum_a K_ad Gu_a ----
@@ -259,6 +296,7 @@ __global__ void __launch_bounds__(bz::THREADS, 1)
             }
         }
       }
+      BZ_MARK(it, 2, lane == 0);
       // ---- GEMM-2 A fragments a[v] = A[cell g + 8v][alpha = 4ks + t] ----
       {
         const int cell = lane & 15;
@@ -299,6 +337,7 @@ __global__ void __launch_bounds__(bz::THREADS, 1)
         fence_proxy_async();
         load(tile + gridDim.x);
       }
+      BZ_MARK(it, 3, lane == 0);
       nbar_arrive(BAR_FULL + b, THREADS);
     }
     return;
@@ -308,7 +347,7 @@ __global__ void __launch_bounds__(bz::THREADS, 1)
   const int ub = c_wblk[warp];
   const int J = bz_J(ub), K = bz_K(ub);
   const bool mirror = J != K;
-  const bool issuer = warp == ISSUER && lane == 0;
+  const bool issuer = warp == ISSUER && lane == 0;  // slab stores + R2 ring refills
   const int hs = g & 1;  // odd-g lanes write the other half first (bank spread)
   // GEMM-1 B fragments of this warp's block: registers for the whole kernel
   double sb[KS1][2];
@@ -316,7 +355,18 @@ __global__ void __launch_bounds__(bz::THREADS, 1)
   for (int ks = 0; ks < KS1; ++ks)
 #pragma unroll
     for (int h = 0; h < 2; ++h) sb[ks][h] = gS[((ub * KS1 + ks) * 2 + h) * 32 + lane];
-  const double2* r2 = reinterpret_cast<const double2*>(gR2) + (size_t)ub * KS2 * 2 * 32 + lane;
+  // GEMM-2 B fragments stream through a ring of k4 stages [25 pairs][32][2]
+  // aliasing slabs 0 and 1 (free while GEMM-2 runs: the last stores of a tile
+  // use slabs 2, 1, 0 in that order and have been read by the time we refill)
+  const int pdir = ub, pmir = NBU + bz_off_index(ub);
+  auto ring_issue = [&](long G) {  // stage G = tile * KS2 + ks -> slot G % NRING
+    const int slot = (int)(G % NRING);
+    const int ks = (int)(G % KS2);
+    mbar_expect_tx(&rFull[slot], STAGE_DBL * 8);
+    bulk_g2s(sRing + slot * STAGE_DBL, gR2 + (size_t)ks * STAGE_DBL, STAGE_DBL * 8, &rFull[slot]);
+  };
+  if (issuer && my_tiles > 0)
+    for (int ks = 0; ks < NRING; ++ks) ring_issue(ks);
 
   long gi = 0;  // running (c,d) block counter of this CTA: slab gi % NSLAB
   for (long it = 0; it < my_tiles; ++it) {
@@ -324,44 +374,38 @@ __global__ void __launch_bounds__(bz::THREADS, 1)
     const int b = (int)(it & 1);
     const double* A1 = sA1 + b * A1_DBL;
     const double* A2 = sA2 + b * A2_DBL;
-    // first GEMM-2 B chunk before waiting for the producer (L2 latency)
-    constexpr int CH = 3;  // k4 steps per register chunk (double-buffered)
-    double2 bq[2][CH][2];
-#pragma unroll
-    for (int kk = 0; kk < CH; ++kk) {
-      bq[0][kk][0] = ldg_nc2(r2 + (kk * 2 + 0) * 32);
-      bq[0][kk][1] = mirror ? ldg_nc2(r2 + (kk * 2 + 1) * 32) : make_double2(0.0, 0.0);
-    }
     nbar_sync(BAR_FULL + b, THREADS);
+    BZ_MARK(it, 4, tid == 0);
 
-    // ---- GEMM-2: C direct (tiles 0,1) and mirror (2,3); B from L2 ----------
+    // ---- GEMM-2: C direct (pair pdir) and mirror (pair pmir) ----------------
     double cdir[2][4], cmir[2][4];
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
       for (int v = 0; v < 4; ++v) cdir[h][v] = cmir[h][v] = 0.0;
-#pragma unroll
-    for (int ch = 0; ch < KS2 / CH; ++ch) {
-      const int cur = ch & 1;
-      if (ch + 1 < KS2 / CH) {
-#pragma unroll
-        for (int kk = 0; kk < CH; ++kk) {
-          const int ks = (ch + 1) * CH + kk;
-          bq[cur ^ 1][kk][0] = ldg_nc2(r2 + (ks * 2 + 0) * 32);
-          bq[cur ^ 1][kk][1] = mirror ? ldg_nc2(r2 + (ks * 2 + 1) * 32) : make_double2(0.0, 0.0);
-        }
+#pragma unroll 2
+    for (int ks = 0; ks < KS2; ++ks) {
+      const long G = it * KS2 + ks;
+      const int slot = (int)(G % NRING);
+      mbar_wait(&rFull[slot], (uint32_t)((G / NRING) & 1));
+      const double2* st = reinterpret_cast<const double2*>(sRing + slot * STAGE_DBL);
+      const double2 bd = st[pdir * 32 + lane];
+      const double2 bm = mirror ? st[pmir * 32 + lane] : make_double2(0.0, 0.0);
+      const double2 af = reinterpret_cast<const double2*>(A2)[ks * 32 + lane];
+      __syncwarp();
+      if (lane == 0) mbar_arrive1(&rEmpty[slot]);
+      dmma16x8x4(cdir[0], af.x, af.y, bd.x);
+      dmma16x8x4(cdir[1], af.x, af.y, bd.y);
+      if (mirror) {
+        dmma16x8x4(cmir[0], af.x, af.y, bm.x);
+        dmma16x8x4(cmir[1], af.x, af.y, bm.y);
       }
-#pragma unroll
-      for (int kk = 0; kk < CH; ++kk) {
-        const double2 af = reinterpret_cast<const double2*>(A2)[(ch * CH + kk) * 32 + lane];
-        dmma16x8x4(cdir[0], af.x, af.y, bq[cur][kk][0].x);
-        dmma16x8x4(cdir[1], af.x, af.y, bq[cur][kk][0].y);
-        if (mirror) {
-          dmma16x8x4(cmir[0], af.x, af.y, bq[cur][kk][1].x);
-          dmma16x8x4(cmir[1], af.x, af.y, bq[cur][kk][1].y);
-        }
+      if (issuer && ks + NRING < KS2) {  // refill the slot with stage ks + NRING
+        mbar_wait(&rEmpty[slot], (uint32_t)((G / NRING) & 1));
+        ring_issue(G + NRING);
       }
     }
+    BZ_MARK(it, 5, tid == 0);
     // odd-g lanes handle half 1 first: swap C once per tile
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
@@ -371,6 +415,7 @@ __global__ void __launch_bounds__(bz::THREADS, 1)
       cmir[0][v] = hs ? m1 : m0;
       cmir[1][v] = hs ? m0 : m1;
     }
+    nbar_sync(BAR_CD, CTHREADS);  // ring reads done before slab 0/1 writes
 
     // ---- the nine (c,d) blocks: GEMM-1, + C on the diagonal, slab, TMA ----
 #pragma unroll 1
@@ -434,11 +479,25 @@ __global__ void __launch_bounds__(bz::THREADS, 1)
         }
       }
       fence_proxy_async();  // generic-proxy slab writes -> visible to the TMA unit
-      if (issuer) bulk_wait_read1();  // slab of block gi-2 free before anyone writes it next
+      if (issuer) {
+        BZ_T0();
+        bulk_wait_read1();  // slab of block gi-2 free before anyone writes it next
+        BZ_ACC(it, 15);
+      }
       nbar_sync(BAR_CD, CTHREADS);
+      BZ_MARK(it, 6 + cdi, tid == 0);
       if (issuer) {
         slab_store(&amap, slab, d * NS, c * NS, (int)c0, acc);
         bulk_commit();
+      }
+    }
+    if (issuer && it + 1 < my_tiles) {
+      // slabs 0 and 1 (stores of steps 6, 7) read out -> first stages of the next tile
+      bulk_wait_read1();
+      for (int k = 0; k < NRING; ++k) {
+        const long G = (it + 1) * KS2 + k;
+        mbar_wait(&rEmpty[G % NRING], (uint32_t)(((G / NRING) - 1) & 1));
+        ring_issue(G);
       }
     }
     if (it + 2 < my_tiles) nbar_arrive(BAR_EMPTY + b, THREADS);
@@ -570,9 +629,11 @@ int burgers_tables(int nq, const double* W, const double* B, const double* D, do
           int j, k;
           jk_of(ub, h, g, &j, &k);
           // direct tile: C[j][k]; mirror tile: the lane writing (k, j) needs C[k][j]
-          r2[(((ub * KS2 + ks) * 2 + 0) * 32 + lane) * 2 + h] = R2[((size_t)al * NS + j) * NS + k];
-          r2[(((ub * KS2 + ks) * 2 + 1) * 32 + lane) * 2 + h] =
-              off ? R2[((size_t)al * NS + k) * NS + j] : 0.0;
+          // [ks][pair][32][2]: direct pair ub, mirror pair 15 + off index
+          r2[((ks * NPAIR + ub) * 32 + lane) * 2 + h] = R2[((size_t)al * NS + j) * NS + k];
+          if (off)
+            r2[((ks * NPAIR + NBU + bz_off_index(ub)) * 32 + lane) * 2 + h] =
+                R2[((size_t)al * NS + k) * NS + j];
         }
   }
   return rank;

@@ -10,6 +10,9 @@ import torch  # noqa: E402
 
 from paper_1604_05872_b200 import fe, femgpu  # noqa: E402
 
+if os.environ.get("FEMGPU_LIB"):  # A/B builds (development)
+    femgpu.LIB_PATH = os.environ["FEMGPU_LIB"]
+
 
 def main(names):
     dev = torch.device("cuda:0")
