@@ -77,7 +77,7 @@ constexpr int STAGE_DBL = NPAIR * 64;         // one k4 step of R2
 constexpr int NRING = 8;                      // ring stages (alias slabs 0 and 1)
 constexpr size_t SMEM =
     sizeof(double) * (size_t)(NSLAB * SLAB_DBL + DN_DBL + 2 * A1_DBL + 2 * A2_DBL + IN_DBL +
-                              CELLS * CELLD) + 8 * (1 + 2 * 8);
+                              CELLS * CELLD) + 8 * (1 + 2 * 8 + 2 * 3);
 static_assert(NRING * STAGE_DBL <= 2 * SLAB_DBL, "R2 ring aliases slabs 0 and 1");
 // named barriers (0 = __syncthreads)
 constexpr int BAR_CD = 1;          // compute warps, once per (c,d) block
@@ -144,6 +144,10 @@ __device__ __forceinline__ void slab_store(const CUtensorMap* map, const double*
         : "memory");
 }
 
+__device__ __forceinline__ void bulk_wait_read2() {
+  asm volatile("cp.async.bulk.wait_group.read 2;\n" ::: "memory");
+}
+
 __device__ __forceinline__ void bulk_wait_read1() {
   asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
 }
@@ -191,6 +195,8 @@ __global__ void __launch_bounds__(bz::THREADS, 1)
   uint64_t* rFull = inBar + 1;             // [NRING] R2 stage landed
   uint64_t* rEmpty = rFull + NRING;        // [NRING] R2 stage consumed by all compute warps
   double* sRing = sSlab;                   // [NRING][25][32][2]  (aliases slabs 0, 1)
+  uint64_t* slabFull = rEmpty + NRING;     // [NSLAB] all compute threads wrote the block
+  uint64_t* slabEmpty = slabFull + NSLAB;  // [NSLAB] the TMA unit has read the slab
   const double* gS = tab;                  // [ub][KS1][2][32]
   const double* gR2 = tab + S_DBL;         // [KS2][25][32][2]
   const double* gDn = gR2 + R2_DBL;        // [3][DNR][20]
@@ -207,6 +213,10 @@ __global__ void __launch_bounds__(bz::THREADS, 1)
     for (int r = 0; r < NRING; ++r) {
       mbar_init(&rFull[r], 1);
       mbar_init(&rEmpty[r], CWARPS);
+    }
+    for (int r = 0; r < NSLAB; ++r) {
+      mbar_init(&slabFull[r], CTHREADS);
+      mbar_init(&slabEmpty[r], 1);
     }
     fence_mbar_init();
   }
@@ -454,6 +464,7 @@ __global__ void __launch_bounds__(bz::THREADS, 1)
             m[hi][v] += cdir[hi][v];
           }
       }
+      if (gi >= NSLAB) mbar_wait(&slabEmpty[gi % NSLAB], (uint32_t)(((gi / NSLAB) - 1) & 1));
       // C fragment c[v] = C[cell g + 8(v>>1)][col 2t + (v&1)];
       // col -> (j, k) = (4J + 2h + t/2, 4K + 2(t&1) + e)
 #pragma unroll
@@ -479,16 +490,20 @@ __global__ void __launch_bounds__(bz::THREADS, 1)
         }
       }
       fence_proxy_async();  // generic-proxy slab writes -> visible to the TMA unit
-      if (issuer) {
-        BZ_T0();
-        bulk_wait_read1();  // slab of block gi-2 free before anyone writes it next
-        BZ_ACC(it, 15);
-      }
-      nbar_sync(BAR_CD, CTHREADS);
+      mbar_arrive1(&slabFull[gi % NSLAB]);
       BZ_MARK(it, 6 + cdi, tid == 0);
       if (issuer) {
+        // the slowest warp gates only this (lightly loaded) warp; the others
+        // run up to two blocks ahead
+        BZ_T0();
+        mbar_wait(&slabFull[gi % NSLAB], (uint32_t)((gi / NSLAB) & 1));
+        BZ_ACC(it, 15);
         slab_store(&amap, slab, d * NS, c * NS, (int)c0, acc);
         bulk_commit();
+        if (gi >= 2) {
+          bulk_wait_read2();  // block gi-2 has left its slab
+          mbar_arrive1(&slabEmpty[(gi - 2) % NSLAB]);
+        }
       }
     }
     if (issuer && it + 1 < my_tiles) {
