@@ -329,7 +329,9 @@ def run_ours(args, rank, world, local):
     F_roof = min(F_exec, Fa) if Fa else F_exec
     bpc = cfg.bytes_per_cell()
     avg_launch_s = (sum(per_launch) / len(per_launch)) / 1e3
-    hbm_bound = args.config in ("c1", "c3")
+    # the bound is whichever floor is longer: algorithmic bytes at the measured HBM
+    # bandwidth or algorithmic flops at the measured FP64 (DMMA) peak
+    hbm_bound = bpc / peaks["hbm_gbs"] >= F_roof / (peaks["fp64_tflops"] * 1e3)
     if hbm_bound:
         achieved = E * bpc / avg_launch_s / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
