@@ -56,7 +56,7 @@ int guarded(Fn&& fn) {
   }
 }
 
-enum Route { ROUTE_HELM_P1, ROUTE_HELM_TENSOR, ROUTE_PAIR, ROUTE_BURGERS };
+enum Route { ROUTE_HELM_P1, ROUTE_HELM_TENSOR, ROUTE_PAIR, ROUTE_ELAS_TENSOR, ROUTE_BURGERS };
 
 std::string two(int m) {
   char b[8];
@@ -299,6 +299,9 @@ void launch(const femgpu_form* f, long E, const double* coords, const double* co
     case ROUTE_PAIR:
       e = femgpu::launch_pair(f->kind, f->nq, f->ns, E, coords, coef, f->d_tab, A, acc, s);
       break;
+    case ROUTE_ELAS_TENSOR:
+      e = femgpu::launch_elas_tensor(E, coords, coef, f->d_tab, A, acc, s);
+      break;
     case ROUTE_BURGERS:
       e = femgpu::launch_burgers(f->ns, E, coords, coef, f->d_tab, f->consts[0], f->consts[1], A,
                                  acc, s);
@@ -353,6 +356,17 @@ int femgpu_form_create(const femgpu_form_desc* d, femgpu_form** out) {
         f->schedule = FEMGPU_SCHED_TENSOR;
         break;
       case FEMGPU_ELASTICITY:
+        if (femgpu::elas_tensor_supported(d->ns, d->nc) && d->schedule == FEMGPU_SCHED_TENSOR) {
+          f->route = ROUTE_ELAS_TENSOR;
+          f->schedule = FEMGPU_SCHED_TENSOR;
+          host.assign(femgpu::elas_tensor_table_doubles(), 0.0);
+          femgpu::elas_tensor_tables(f->nq, f->W.data(), f->D.data(), f->P.data(), host.data());
+          // alpha: 6 blocks x 36 x 3; GEMM: 3 full 10x10 + 3 upper halves (55) x 36 x 2
+          f->flops_per_cell = 60 + 6.0 * 36 * 3 + 2.0 * 36 * (3 * 100 + 3 * 55);
+          f->kernel_name = "elas_tensor_kernel";
+          break;
+        }
+        [[fallthrough]];
       case FEMGPU_HYPERELASTICITY: {
         if (!femgpu::pair_supported(d->kind, d->nq, d->ns) || d->schedule == FEMGPU_SCHED_TENSOR)
           throw Error(FEMGPU_ERR_UNSUPPORTED, "no vector-form kernel for this size/schedule");

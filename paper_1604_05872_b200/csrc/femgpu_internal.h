@@ -32,6 +32,13 @@ cudaError_t launch_pair(int kind, int nq, int ns, long E, const double* coords,
                         const double* coef, const double* tab, double* A, int acc,
                         cudaStream_t s);
 
+// Linear elasticity tensor schedule (see elasticity.cu).
+bool elas_tensor_supported(int ns, int nc);
+size_t elas_tensor_table_doubles();
+void elas_tensor_tables(int nq, const double* W, const double* D, const double* P, double* out);
+cudaError_t launch_elas_tensor(long E, const double* coords, const double* coef, const double* tab,
+                               double* A, int acc, cudaStream_t s);
+
 // Burgers tensor schedule (see burgers.cu).
 bool burgers_supported(int nq, int ns);
 size_t burgers_table_doubles();

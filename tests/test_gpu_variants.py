@@ -56,18 +56,52 @@ def test_variant_parity(name):
     assert np.abs(A - A.transpose(0, 2, 1)).max() <= 1e-13 * np.abs(A).max()
 
 
+def test_elasticity_tensor_accumulate_and_ragged():
+    import port
+
+    cfg = fe.CONFIGS["c3"]
+    tabs = fe.tables(cfg)
+    form = femgpu.Form.from_config(cfg, tabs, schedule=femgpu.SCHED_TENSOR)
+    dev = torch.device("cuda:0")
+    for E in (1, 4, 6, 11, 37):
+        coords, coeffs = fe.cell_inputs(cfg, ncells=E)
+        R = port.assemble(cfg, tabs, coords, coeffs)
+        x = torch.from_numpy(coords).to(dev)
+        c = torch.from_numpy(coeffs).to(dev)
+        out = torch.full((E, cfg.n, cfg.n), 1.5, dtype=torch.float64, device=dev)
+        form.assemble(x, c, out, accumulate=True)
+        torch.cuda.synchronize()
+        assert frob_rel(out.cpu().numpy() - 1.5, R) < 1e-11
+
+
 def test_schedule_contract():
-    # Helmholtz has only the tensor schedule; vector forms only the quadrature one
+    # Helmholtz has only the tensor schedule, St Venant-Kirchhoff only the
+    # quadrature one; elasticity has both (auto = quadrature, the faster one)
     with pytest.raises(femgpu.FemgpuError) as e:
         femgpu.Form.from_config(fe.CONFIGS["c2"], schedule=femgpu.SCHED_QUADRATURE)
     assert e.value.code == 14
     with pytest.raises(femgpu.FemgpuError) as e:
-        femgpu.Form.from_config(fe.CONFIGS["c3"], schedule=femgpu.SCHED_TENSOR)
+        femgpu.Form.from_config(fe.CONFIGS["c4"], schedule=femgpu.SCHED_TENSOR)
     assert e.value.code == 14
     f = femgpu.Form.from_config(fe.CONFIGS["c2"], schedule=femgpu.SCHED_TENSOR)
     assert f.info["schedule"] == "tensor"
     f = femgpu.Form.from_config(fe.CONFIGS["c4"], schedule=femgpu.SCHED_QUADRATURE)
     assert f.info["schedule"] == "quadrature"
+    f = femgpu.Form.from_config(fe.CONFIGS["c3"])
+    assert f.info["schedule"] == "quadrature"
+    f = femgpu.Form.from_config(fe.CONFIGS["c3"], schedule=femgpu.SCHED_TENSOR)
+    assert f.info["schedule"] == "tensor" and f.info["kernel_name"] == "elas_tensor_kernel"
+
+
+@pytest.mark.parametrize("name", ["c3", "elas_q27"])
+def test_elasticity_tensor_schedule(name):
+    # the DMMA pre-evaluated kernel (elasticity.cu), on request
+    cfg = fe.CONFIGS["c3"] if name == "c3" else VARIANTS[name]
+    cfg = replace(cfg, N=4)
+    form, A, R = run(cfg, schedule=femgpu.SCHED_TENSOR)
+    assert form.info["kernel_name"] == "elas_tensor_kernel"
+    assert frob_rel(A, R) < TOL
+    assert np.abs(A - A.transpose(0, 2, 1)).max() <= 1e-13 * np.abs(A).max()
 
 
 def test_unsupported_shapes_fail_loudly():
