@@ -41,11 +41,16 @@
 #include "femgpu_internal.h"
 #include "../../include/femgpu.h"
 
+#ifndef PAIR_QUNROLL
+#define PAIR_QUNROLL 4  // q-loop unroll of the accumulate phase (measured: 1.56 -> 1.48 ms on c4)
+#endif
 #ifndef PAIR_ELAS_FLAT
 #define PAIR_ELAS_FLAT 0
 #endif
 
 namespace femgpu {
+
+constexpr int kPairQUnroll = PAIR_QUNROLL;
 
 template <int KIND, int NS, int Q>
 struct PairShape {
@@ -564,7 +569,7 @@ __global__ void __launch_bounds__(128, 2)
       __syncthreads();
       if (ch == Sh::NCHUNK - 1 && tile + gridDim.x < ntiles) prefetch(tile + gridDim.x);
       if (sl.active) {
-#pragma unroll 1
+#pragma unroll kPairQUnroll
         for (int ql = 0; ql < qn; ++ql)
           pair_point<Sh>(a4, sU + ql * NS * Sh::JS + sl.cell, sQs + ql * Sh::QSD * CELLS + sl.cell,
                          sl.j0, sl.k0);
