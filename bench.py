@@ -159,6 +159,21 @@ def profile_traffic(cfg_name):
         return None
 
 
+def ncu_flops(cfg_name, kernel_name):
+    """F_exec as SURVEY.md §8d defines it: FP64 flops executed per cell, counted by
+    ncu (tools/ncu_flops.py; DFMA = 2, DADD/DMUL = 1, DMMA = 2mnk), if the committed
+    capture is of the kernel this form runs."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            d = json.load(f).get(cfg_name, {})
+    except (OSError, ValueError):
+        return None
+    k = d.get("fp64_flops_ncu_kernel") or ""
+    base = kernel_name.split("<")[0]
+    ok = base in k or (base == "pair_kernel" and "pair_" in k)
+    return d.get("fp64_flops_per_cell_ncu") if ok else None
+
+
 # ----------------------------------------------------------------------------
 def cpu_reference_rate(cfg, seconds: float, nthreads: int, coords, coeffs):
     """The reference's CPU path (femopt-optimized emitted C, oracle/_ref) on a
@@ -324,7 +339,9 @@ def run_ours(args, rank, world, local):
     if rank != 0:
         return
     peaks = load_peaks()
-    F_exec = form.info["flops_per_cell"]
+    F_model = form.info["flops_per_cell"]
+    F_ncu = ncu_flops(args.config, form.info["kernel_name"])
+    F_exec = F_ncu if F_ncu else F_model
     Fa = f_alg(args.config)
     F_roof = min(F_exec, Fa) if Fa else F_exec
     bpc = cfg.bytes_per_cell()
@@ -356,7 +373,10 @@ def run_ours(args, rank, world, local):
                    "l2": "inputs+outputs per step > 126 MB L2 (no flush needed)",
                    "kernel": form.info["kernel_name"], "schedule": form.info["schedule"]},
         "gflops": value * F_roof / 1e9,
-        "flops_per_cell": {"F_exec_model": F_exec, "F_alg_reference": Fa, "F_roof": F_roof},
+        "flops_per_cell": {"F_exec_ncu": F_ncu, "F_exec_model": F_model, "F_alg_reference": Fa,
+                           "F_roof": F_roof,
+                           "rule": "F_roof = min(F_alg, F_exec); F_exec = ncu-counted FP64 flops "
+                                   "(profiles/ncu_flops_r01) when present, else the kernel's model"},
         "bytes_per_cell": bpc,
         "roofline": roof,
         "roofline_step_frac": t_roof / (ms_per_step / 1e3),

@@ -76,7 +76,7 @@ def main():
         cfg, path = arg.split("=", 1)
         r = summarise(path)
         r["capture"] = f"{tag}: ncu --set full --clock-control none (1 launch, cold)"
-        allres[cfg] = r
+        allres.setdefault(cfg, {}).update(r)  # keep other tools' fields (ncu_flops.py)
         print(cfg, json.dumps(r))
     with open(dst, "w") as f:
         json.dump(allres, f, indent=1, sort_keys=True)
