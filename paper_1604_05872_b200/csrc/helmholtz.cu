@@ -280,9 +280,9 @@ __global__ void __launch_bounds__(HelmTensorShape<NS, NC>::THREADS, 1)
           double a[Sh::MT][4];
 #pragma unroll
           for (int mt = 0; mt < Sh::MT; ++mt) {
-            const double2* ap =
-                reinterpret_cast<const double2*>(&sAb[((mt * Sh::KS + ks) * 32 + lane) * 4]);
-            const double2 a01 = ap[0], a23 = ap[1];
+            // [mt][ks][half][32 lanes][2]: each 16-byte load is lane-contiguous
+            const double2* ap = reinterpret_cast<const double2*>(sAb) + (mt * Sh::KS + ks) * 64 + lane;
+            const double2 a01 = ap[0], a23 = ap[32];
             a[mt][0] = a01.x;
             a[mt][1] = a01.y;
             a[mt][2] = a23.x;
@@ -382,14 +382,14 @@ __global__ void __launch_bounds__(HelmTensorShape<NS, NC>::THREADS, 1)
               const int alpha = m * 7 + s;
               const int ks = alpha >> 3, kk = alpha & 7;
               const int ln = gg * 4 + (kk & 3), v = vrow + 2 * (kk >> 2);
-              sAb[((cmt * Sh::KS + ks) * 32 + ln) * 4 + v] = fv[i] * Gs[s];
+              sAb[(((cmt * Sh::KS + ks) * 2 + (v >> 1)) * 32 + ln) * 2 + (v & 1)] = fv[i] * Gs[s];
             }
           }
         }
         for (int alpha = Sh::KR + part; alpha < 8 * Sh::KS; alpha += PARTS) {  // zero K padding
           const int ks = alpha >> 3, kk = alpha & 7;
           const int ln = gg * 4 + (kk & 3), v = vrow + 2 * (kk >> 2);
-          sAb[((cmt * Sh::KS + ks) * 32 + ln) * 4 + v] = 0.0;
+          sAb[(((cmt * Sh::KS + ks) * 2 + (v >> 1)) * 32 + ln) * 2 + (v & 1)] = 0.0;
         }
       }
       io_barrier(Sh::IO_THREADS);  // sIn free for the next prologue
