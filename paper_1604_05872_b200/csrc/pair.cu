@@ -387,30 +387,34 @@ __global__ void __launch_bounds__(PairShape<FEMGPU_ELASTICITY, NS, Q>::THREADS, 
       if (it >= 2) mbar_wait(&empty[b], (uint32_t)(((it >> 1) - 1) & 1));
       double* rec = sRec + b * Sh::REC_DBL;
       double* qsb = rec + Q * NS * Sh::JS;
-      for (int task = pt; task < CELLS * Q * NS; task += Sh::PROD) {
-        const int c = task % CELLS, r = task / CELLS;
-        const int j = r % NS, q = r / NS;
-        const double* K = sCell + c * Sh::CELLD;
-        double* rr = rec + (q * NS + j) * Sh::JS + c;
+      // thread -> (cell, q): K, mu', lam' once, then the 10 records g_j = K^T D phi_j
+      for (int task = pt; task < CELLS * Q; task += Sh::PROD) {
+        const int c = task % CELLS, q = task / CELLS;
+        const double* Kp = sCell + c * Sh::CELLD;
+        double K[9];
 #pragma unroll
-        for (int bb = 0; bb < 3; ++bb)
-          rr[bb * CELLS] = K[0 * 3 + bb] * sD[(0 * Q + q) * NS + j] +
-                           K[1 * 3 + bb] * sD[(1 * Q + q) * NS + j] +
-                           K[2 * 3 + bb] * sD[(2 * Q + q) * NS + j];
-        if (j == 0) {
-          const double* cf = in + CELLS * 12 + c * Sh::NCOEF;
-          double muq = 0, lamq = 0;
-          if (c < nt) {
+        for (int i = 0; i < 9; ++i) K[i] = Kp[i];
+        const double* cf = in + CELLS * 12 + c * Sh::NCOEF;
+        double muq = 0, lamq = 0;
+        if (c < nt) {
 #pragma unroll
-            for (int m = 0; m < 4; ++m) {
-              muq += cf[m] * sP[q * 4 + m];
-              lamq += cf[4 + m] * sP[q * 4 + m];
-            }
+          for (int m = 0; m < 4; ++m) {
+            muq += cf[m] * sP[q * 4 + m];
+            lamq += cf[4 + m] * sP[q * 4 + m];
           }
-          const double wq = sW[q] * K[9];
-          double* qs = qsb + q * Sh::QSD * CELLS + c;
-          qs[0] = lamq * wq;
-          qs[CELLS] = muq * wq;
+        }
+        const double wq = sW[q] * Kp[9];
+        double* qs = qsb + q * Sh::QSD * CELLS + c;
+        qs[0] = lamq * wq;
+        qs[CELLS] = muq * wq;
+        double* rr = rec + q * NS * Sh::JS + c;
+#pragma unroll 5
+        for (int j = 0; j < NS; ++j) {
+          const double d0 = sD[(0 * Q + q) * NS + j], d1 = sD[(1 * Q + q) * NS + j],
+                       d2 = sD[(2 * Q + q) * NS + j];
+#pragma unroll
+          for (int bb = 0; bb < 3; ++bb)
+            rr[j * Sh::JS + bb * CELLS] = K[0 * 3 + bb] * d0 + K[1 * 3 + bb] * d1 + K[2 * 3 + bb] * d2;
         }
       }
       mbar_arrive_cta(&full[b]);  // release: this tile's records are visible
