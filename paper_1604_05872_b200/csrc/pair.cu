@@ -129,8 +129,8 @@ __device__ __forceinline__ PairSlot pair_slot(int tid) {
 
 // Accumulate one quadrature point's records into the thread's 2x2 tile.
 template <class Sh>
-__device__ __forceinline__ void pair_point(double (&a4)[2][2][3][3], const double* rq,
-                                           const double* qs, int j0, int k0) {
+__device__ __forceinline__ void pair_point(double (&a4)[2][2][3][3], double (&t1)[2][2],
+                                           const double* rq, const double* qs, int j0, int k0) {
   constexpr int CELLS = Sh::CELLS, JS = Sh::JS;
   const double lq = qs[0], mq = qs[CELLS];
   double gk[2][3];
@@ -174,6 +174,7 @@ __device__ __forceinline__ void pair_point(double (&a4)[2][2][3][3], const doubl
     for (int y = 0; y < 2; ++y)
 #pragma unroll
       for (int bb = 0; bb < 3; ++bb) hk[y][bb] = rq[(k0 + y) * JS + (3 + bb) * CELLS];
+    // qs holds mu' F F^T (pre-scaled in the setup), so g_j enters unscaled
     const double f00 = qs[2 * CELLS], f01 = qs[3 * CELLS], f02 = qs[4 * CELLS];
     const double f11 = qs[5 * CELLS], f12 = qs[6 * CELLS], f22 = qs[7 * CELLS];
     const double ff[3][3] = {{f00, f01, f02}, {f01, f11, f12}, {f02, f12, f22}};
@@ -183,16 +184,17 @@ __device__ __forceinline__ void pair_point(double (&a4)[2][2][3][3], const doubl
       const double* r = rq + (j0 + x) * JS;
 #pragma unroll
       for (int bb = 0; bb < 3; ++bb) {
-        gj[bb] = mq * r[bb * CELLS];           // mu' g_j
+        gj[bb] = r[bb * CELLS];                // g_j
         const double h = r[(3 + bb) * CELLS];
         lh[bb] = lq * h;                       // lam' h_j
         mh[bb] = mq * h;                       // mu' h_j
         s[bb] = r[(6 + bb) * CELLS];           // w' S g_j
       }
-      double t1[2], t2[2];
+      double t2[2];
 #pragma unroll
       for (int y = 0; y < 2; ++y) {
-        t1[y] = s[0] * gk[y][0] + s[1] * gk[y][1] + s[2] * gk[y][2];
+        // s_j.g_k accumulates over q on its own; added to the (c,c) entries once
+        t1[x][y] = fma(s[0], gk[y][0], fma(s[1], gk[y][1], fma(s[2], gk[y][2], t1[x][y])));
         t2[y] = gj[0] * gk[y][0] + gj[1] * gk[y][1] + gj[2] * gk[y][2];
       }
 #pragma unroll
@@ -213,12 +215,18 @@ __device__ __forceinline__ void pair_point(double (&a4)[2][2][3][3], const doubl
         for (int c = 0; c < 3; ++c)
 #pragma unroll
           for (int d = 0; d < 3; ++d) a4[x][y][c][d] = fma(t2[y], ff[c][d], a4[x][y][c][d]);
-#pragma unroll
-      for (int y = 0; y < 2; ++y)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) a4[x][y][c][c] += t1[y];
     }
   }
+}
+
+// SVK: the accumulated s_j.g_k enters the (c,c) entries of each (j,k) pair.
+__device__ __forceinline__ void add_t1(double (&a4)[2][2][3][3], const double (&t1)[2][2]) {
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int y = 0; y < 2; ++y)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) a4[x][y][c][c] += t1[x][y];
 }
 
 // The tile's symmetric half, mirrored, into the cell's staging row.
@@ -325,6 +333,7 @@ __global__ void __launch_bounds__(PairShape<FEMGPU_ELASTICITY, NS, Q>::THREADS, 
       const int nt = (int)min((long)CELLS, E - c0);
       const int b = (int)(it & 1);
       double a4[2][2][3][3];
+      double t1[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // SVK only (unused for elasticity)
       zero_tile(a4);
       mbar_wait(&full[b], (uint32_t)((it >> 1) & 1));
       const double* rec = sRec + b * Sh::REC_DBL;
@@ -332,8 +341,8 @@ __global__ void __launch_bounds__(PairShape<FEMGPU_ELASTICITY, NS, Q>::THREADS, 
       if (sl.active) {
 #pragma unroll 1
         for (int q = 0; q < Q; ++q)
-          pair_point<Sh>(a4, rec + q * NS * Sh::JS + sl.cell, qsb + q * Sh::QSD * CELLS + sl.cell,
-                         sl.j0, sl.k0);
+          pair_point<Sh>(a4, t1, rec + q * NS * Sh::JS + sl.cell,
+                         qsb + q * Sh::QSD * CELLS + sl.cell, sl.j0, sl.k0);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive_cta(&empty[b]);
@@ -480,6 +489,7 @@ __global__ void __launch_bounds__(128, 2)
       return c < nt ? sIn[CELLS * 12 + c * Sh::NCOEF + r] : 0.0;
     };
     double a4[2][2][3][3];
+    double t1[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // SVK: sum_q s_j.g_k
     zero_tile(a4);
 #pragma unroll 1
     for (int ch = 0; ch < Sh::NCHUNK; ++ch) {
@@ -546,12 +556,13 @@ __global__ void __launch_bounds__(128, 2)
           for (int b = 0; b < 3; ++b)
             Sw[a][b] = wq * ((a == b ? lamq * trE : 0.0) + 2.0 * muq * Ee[a][b]);
         // F F^T: (0,0),(0,1),(0,2),(1,1),(1,2),(2,2)
-        qs[2 * CELLS] = F[0][0] * F[0][0] + F[0][1] * F[0][1] + F[0][2] * F[0][2];
-        qs[3 * CELLS] = F[0][0] * F[1][0] + F[0][1] * F[1][1] + F[0][2] * F[1][2];
-        qs[4 * CELLS] = F[0][0] * F[2][0] + F[0][1] * F[2][1] + F[0][2] * F[2][2];
-        qs[5 * CELLS] = F[1][0] * F[1][0] + F[1][1] * F[1][1] + F[1][2] * F[1][2];
-        qs[6 * CELLS] = F[1][0] * F[2][0] + F[1][1] * F[2][1] + F[1][2] * F[2][2];
-        qs[7 * CELLS] = F[2][0] * F[2][0] + F[2][1] * F[2][1] + F[2][2] * F[2][2];
+        const double mw = muq * wq;  // mu' F F^T: pre-scaled for the accumulate phase
+        qs[2 * CELLS] = mw * (F[0][0] * F[0][0] + F[0][1] * F[0][1] + F[0][2] * F[0][2]);
+        qs[3 * CELLS] = mw * (F[0][0] * F[1][0] + F[0][1] * F[1][1] + F[0][2] * F[1][2]);
+        qs[4 * CELLS] = mw * (F[0][0] * F[2][0] + F[0][1] * F[2][1] + F[0][2] * F[2][2]);
+        qs[5 * CELLS] = mw * (F[1][0] * F[1][0] + F[1][1] * F[1][1] + F[1][2] * F[1][2]);
+        qs[6 * CELLS] = mw * (F[1][0] * F[2][0] + F[1][1] * F[2][1] + F[1][2] * F[2][2]);
+        qs[7 * CELLS] = mw * (F[2][0] * F[2][0] + F[2][1] * F[2][1] + F[2][2] * F[2][2]);
 #pragma unroll 2
         for (int j = 0; j < NS; ++j) {
           double g[3];
@@ -575,11 +586,12 @@ __global__ void __launch_bounds__(128, 2)
       if (sl.active) {
 #pragma unroll kPairQUnroll
         for (int ql = 0; ql < qn; ++ql)
-          pair_point<Sh>(a4, sU + ql * NS * Sh::JS + sl.cell, sQs + ql * Sh::QSD * CELLS + sl.cell,
-                         sl.j0, sl.k0);
+          pair_point<Sh>(a4, t1, sU + ql * NS * Sh::JS + sl.cell,
+                         sQs + ql * Sh::QSD * CELLS + sl.cell, sl.j0, sl.k0);
       }
       __syncthreads();  // records consumed (next chunk / staging overwrite them)
     }
+    if constexpr (Sh::SVK) add_t1(a4, t1);
     if (sl.active) pair_stage<Sh>(sU + sl.cell * Sh::CSTRIDE, a4, sl);
     fence_proxy_async();
     __syncthreads();
