@@ -161,12 +161,10 @@ __device__ __forceinline__ void pair_point(double (&a4)[2][2][3][3], double (&t1
         for (int c = 0; c < 3; ++c)
 #pragma unroll
           for (int d = 0; d < 3; ++d) a4[x][y][c][d] = fma(u[d], gk[y][c], a4[x][y][c][d]);
+      // mu' g_j.g_k accumulates over q on its own; added to the (c,c) entries once
 #pragma unroll
-      for (int y = 0; y < 2; ++y) {
-        const double S = u[0] * gk[y][0] + u[1] * gk[y][1] + u[2] * gk[y][2];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) a4[x][y][c][c] += S;
-      }
+      for (int y = 0; y < 2; ++y)
+        t1[x][y] = fma(u[0], gk[y][0], fma(u[1], gk[y][1], fma(u[2], gk[y][2], t1[x][y])));
     }
   } else {
     double hk[2][3];
@@ -219,7 +217,8 @@ __device__ __forceinline__ void pair_point(double (&a4)[2][2][3][3], double (&t1
   }
 }
 
-// SVK: the accumulated s_j.g_k enters the (c,c) entries of each (j,k) pair.
+// The q-summed scalar term (SVK s_j.g_k, elasticity mu' g_j.g_k) enters the
+// (c,c) entries of each (j,k) pair once.
 __device__ __forceinline__ void add_t1(double (&a4)[2][2][3][3], const double (&t1)[2][2]) {
 #pragma unroll
   for (int x = 0; x < 2; ++x)
@@ -333,7 +332,7 @@ __global__ void __launch_bounds__(PairShape<FEMGPU_ELASTICITY, NS, Q>::THREADS, 
       const int nt = (int)min((long)CELLS, E - c0);
       const int b = (int)(it & 1);
       double a4[2][2][3][3];
-      double t1[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // SVK only (unused for elasticity)
+      double t1[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // sum_q mu' g_j.g_k
       zero_tile(a4);
       mbar_wait(&full[b], (uint32_t)((it >> 1) & 1));
       const double* rec = sRec + b * Sh::REC_DBL;
@@ -348,6 +347,7 @@ __global__ void __launch_bounds__(PairShape<FEMGPU_ELASTICITY, NS, Q>::THREADS, 
       if (lane == 0) mbar_arrive_cta(&empty[b]);
       if (tid == 0) bulk_wait_read0();  // previous tile's bulk stores have read the staging
       named_bar(1, Sh::ACC);
+      add_t1(a4, t1);
       if (sl.active) pair_stage<Sh>(sStg + sl.cell * Sh::CSTRIDE, a4, sl);
       fence_proxy_async();
       named_bar(1, Sh::ACC);
@@ -489,7 +489,7 @@ __global__ void __launch_bounds__(128, 2)
       return c < nt ? sIn[CELLS * 12 + c * Sh::NCOEF + r] : 0.0;
     };
     double a4[2][2][3][3];
-    double t1[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // SVK: sum_q s_j.g_k
+    double t1[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // SVK: sum_q s_j.g_k; elasticity: mu' g_j.g_k
     zero_tile(a4);
 #pragma unroll 1
     for (int ch = 0; ch < Sh::NCHUNK; ++ch) {
@@ -591,7 +591,7 @@ __global__ void __launch_bounds__(128, 2)
       }
       __syncthreads();  // records consumed (next chunk / staging overwrite them)
     }
-    if constexpr (Sh::SVK) add_t1(a4, t1);
+    add_t1(a4, t1);
     if (sl.active) pair_stage<Sh>(sU + sl.cell * Sh::CSTRIDE, a4, sl);
     fence_proxy_async();
     __syncthreads();
