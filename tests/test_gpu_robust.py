@@ -1,0 +1,108 @@
+"""GPU robustness beyond the BASELINE meshes: inverted cells, element-matrix
+index ranges past 2^31 doubles, and launches on several streams at once.
+Checked against the C oracle (pinned to the reference by tests/test_oracle.py)."""
+import threading
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_1604_05872_b200 import fe, femgpu  # noqa: E402
+
+TOL = 1e-12
+CONFIGS = ["c1", "c2", "c3", "c4", "c5"]
+
+
+def frob_rel(A, R):
+    A = np.asarray(A).reshape(len(A), -1)
+    R = np.asarray(R).reshape(len(R), -1)
+    return float(np.max(np.linalg.norm(A - R, axis=1) / np.linalg.norm(R, axis=1)))
+
+
+@pytest.mark.parametrize("name", CONFIGS)
+def test_inverted_cells(name):
+    # negative Jacobian determinant on every other cell (vertices 1 and 2
+    # swapped): the forms integrate with |det J|, like the reference IR
+    import port
+
+    cfg = fe.CONFIGS[name]
+    tabs = fe.tables(cfg)
+    coords, coeffs = fe.cell_inputs(cfg, ncells=67)
+    x = coords.reshape(-1, 4, 3).copy()
+    x[::2, [1, 2]] = x[::2, [2, 1]]
+    coords = x.reshape(-1, 12)
+    form = femgpu.Form.from_config(cfg, tabs)
+    dev = torch.device("cuda:0")
+    out = torch.empty((coords.shape[0], cfg.n, cfg.n), dtype=torch.float64, device=dev)
+    form.assemble(torch.from_numpy(coords).to(dev), torch.from_numpy(coeffs).to(dev), out)
+    torch.cuda.synchronize()
+    assert frob_rel(out.cpu().numpy(), port.assemble(cfg, tabs, coords, coeffs)) < TOL
+
+
+def _device_inputs(cfg, E, dev, seed=7):
+    """E jittered unit-scale tetrahedra and coefficient dofs, generated on the device."""
+    g = torch.Generator(device=dev).manual_seed(seed)
+    ref = torch.tensor([0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0, 1], dtype=torch.float64, device=dev)
+    coords = ref + 0.1 * (torch.rand((E, 12), generator=g, dtype=torch.float64, device=dev) - 0.5)
+    coeffs = 0.5 + torch.rand((E, cfg.ncoef), generator=g, dtype=torch.float64, device=dev)
+    if cfg.kind == fe.HYPERELASTICITY:  # small displacement dofs
+        coeffs[:, : 3 * cfg.ns] = 0.1 * (coeffs[:, : 3 * cfg.ns] - 1.0)
+    return coords, coeffs
+
+
+@pytest.mark.parametrize("name", ["c1", "c5"])
+def test_element_matrix_index_past_2_31(name):
+    # E * n * n > 2^31 doubles: 64-bit offsets in every kernel's output path
+    import port
+
+    cfg = fe.CONFIGS[name]
+    E = (1 << 31) // (cfg.n * cfg.n) + 4099
+    dev = torch.device("cuda:0")
+    free, _ = torch.cuda.mem_get_info()
+    need = E * (cfg.n * cfg.n + 12 + cfg.ncoef) * 8
+    if need > 0.8 * free:
+        pytest.skip("not enough device memory")
+    coords, coeffs = _device_inputs(cfg, E, dev)
+    out = torch.empty((E, cfg.n, cfg.n), dtype=torch.float64, device=dev)
+    out[-300:] = float("nan")
+    tabs = fe.tables(cfg)
+    form = femgpu.Form.from_config(cfg, tabs)
+    form.assemble(coords, coeffs, out)
+    torch.cuda.synchronize()
+    idx = np.r_[0:3, E // 2, E - 300:E]
+    R = port.assemble(cfg, tabs, coords[idx].cpu().numpy(), coeffs[idx].cpu().numpy())
+    assert frob_rel(out[idx].cpu().numpy(), R) < TOL
+
+
+def test_concurrent_streams_and_threads():
+    # one form per thread, each on its own stream; the form handle's device
+    # tables are shared read-only state
+    import port
+
+    results = {}
+    dev = torch.device("cuda:0")
+
+    def run(name):
+        cfg = fe.CONFIGS[name]
+        tabs = fe.tables(cfg)
+        coords, coeffs = fe.cell_inputs(cfg, ncells=301)
+        form = femgpu.Form.from_config(cfg, tabs)
+        s = torch.cuda.Stream(device=dev)
+        with torch.cuda.stream(s):
+            x = torch.from_numpy(coords).to(dev, non_blocking=False)
+            c = torch.from_numpy(coeffs).to(dev, non_blocking=False)
+            out = torch.empty((coords.shape[0], cfg.n, cfg.n), dtype=torch.float64, device=dev)
+            for _ in range(3):
+                form.assemble(x, c, out, stream=s.cuda_stream)
+        s.synchronize()
+        results[name] = frob_rel(out.cpu().numpy(), port.assemble(cfg, tabs, coords, coeffs))
+
+    threads = [threading.Thread(target=run, args=(n,)) for n in CONFIGS]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert set(results) == set(CONFIGS)
+    assert max(results.values()) < TOL, results
