@@ -308,9 +308,160 @@ def burgers_block(cfg, coords, coeffs, tabs, c, d, encoding="ufl"):
     return k
 
 
+# ----------------------------------------------------------------------------
+# Arity-1 kernels: element vectors (femopt validates
+# linear nests of arity 1, kernel.cpp:369-390)
+# ----------------------------------------------------------------------------
+
+
+def base_vector(E, Q, n, out="b"):
+    return {
+        "indices": {"e": E, "i": Q, "j": n},
+        "loops": [{"index": "e", "class": "orderfree"}, {"index": "i"}, {"index": "j"}],
+        "tables": {},
+        "constants": {},
+        "statements": geometry_statements(),
+        "outputs": [out],
+    }
+
+
+def helmholtz_load(cfg, coords, coeffs, tabs):
+    """Load vector of the Helmholtz configs: b_j = int f phi_j."""
+    E, Q, n = coords.shape[0], tabs.W.shape[0], cfg.ns
+    nc = tabs.P.shape[1]
+    k = base_vector(E, Q, n, "b")
+    T = k["tables"]
+    T.update(geometry_tables(coords))
+    T["W"] = table(["i"], tabs.W)
+    T["B"] = table(["i", "j"], tabs.B)
+    fn = [f"f{m:02d}" for m in range(nc)]
+    pn = [f"P{m:02d}" for m in range(nc)]
+    for m in range(nc):
+        T[fn[m]] = table(["e"], coeffs[:, m])
+        T[pn[m]] = table(["i"], tabs.P[:, m])
+    rhs = mul(coef_sum(fn, pn), S("B", "i", "j"), S("W", "i"), "adet")
+    k["statements"].append(stmt(3, ["b", "e", "j"], rhs, "+="))
+    return k
+
+
+def hyperelasticity_residual(cfg, coords, coeffs, tabs):
+    """St Venant--Kirchhoff internal virtual work r_(c,j) = int (F S) : grad(phi_j e_c),
+    the residual whose Jacobian is ``hyperelasticity`` (F, E, S as there)."""
+    E, Q, ns = coords.shape[0], tabs.W.shape[0], cfg.ns
+    k = base_vector(E, Q, 3 * ns, "r")
+    T = k["tables"]
+    T.update(geometry_tables(coords))
+    T["W"] = table(["i"], tabs.W)
+    for name, v in _padded(tabs, ns).items():
+        T[name] = table(["i", "j"], v)
+    for m in range(4):
+        T[f"P{m}"] = table(["i"], tabs.P[:, m])
+        T[f"mu{m}"] = table(["e"], coeffs[:, 3 * ns + m])
+        T[f"lam{m}"] = table(["e"], coeffs[:, 3 * ns + 4 + m])
+    for a in range(3):
+        for m in range(ns):
+            T[f"Dw{a}{m:02d}"] = table(["i"], tabs.D[a][:, m])
+    for c in range(3):
+        for m in range(ns):
+            T[f"w{c}{m:02d}"] = table(["e"], coeffs[:, c * ns + m])
+    st = k["statements"]
+    st.append(stmt(2, "muq", coef_sum([f"mu{m}" for m in range(4)], [f"P{m}" for m in range(4)])))
+    st.append(stmt(2, "lamq", coef_sum([f"lam{m}" for m in range(4)], [f"P{m}" for m in range(4)])))
+    for c in range(3):
+        for b in range(3):
+            gw = add(*[mul(S(f"w{c}{m:02d}", "e"),
+                           add(*[mul(f"K{a}{b}", S(f"Dw{a}{m:02d}", "i")) for a in range(3)]))
+                       for m in range(ns)])
+            st.append(stmt(2, f"F{c}{b}", add(1.0, gw) if c == b else gw))
+    for a in range(3):
+        for b in range(3):
+            ftf = add(*[mul(f"F{p}{a}", f"F{p}{b}") for p in range(3)])
+            st.append(stmt(2, f"E{a}{b}", mul(0.5, add(ftf, -1.0) if a == b else ftf)))
+    st.append(stmt(2, "trE", add("E00", "E11", "E22")))
+    for a in range(3):
+        for b in range(3):
+            s2 = mul(2.0, "muq", f"E{a}{b}")
+            st.append(stmt(2, f"S{a}{b}", add(mul("lamq", "trE"), s2) if a == b else s2))
+    for c in range(3):
+        for b in range(3):
+            st.append(stmt(2, f"Pk{c}{b}", add(*[mul(f"F{c}{q}", f"S{q}{b}") for q in range(3)])))
+
+    def g(c, b):
+        return grad(lambda a: f"Dv{c}{a}", "j", b)
+
+    rhs = mul(add(*[mul(f"Pk{c}{b}", g(c, b)) for c in range(3) for b in range(3)]),
+              S("W", "i"), "adet")
+    st.append(stmt(3, ["r", "e", "j"], rhs, "+="))
+    return k
+
+
+def burgers_residual(cfg, coords, coeffs, tabs):
+    """Burgers residual r_(c,j) = int (u_c/dt + (u.grad) u_c) phi_j + nu grad u_c . grad phi_j,
+    whose Jacobian is the ``burgers_block`` kernels."""
+    E, Q, ns = coords.shape[0], tabs.W.shape[0], cfg.ns
+    k = base_vector(E, Q, 3 * ns, "r")
+    T = k["tables"]
+    T.update(geometry_tables(coords))
+    T["W"] = table(["i"], tabs.W)
+    for c in range(3):
+        v = np.zeros((Q, 3 * ns))
+        v[:, c * ns:(c + 1) * ns] = tabs.B
+        T[f"Bv{c}"] = table(["i", "j"], v)
+    for name, v in _padded(tabs, ns).items():
+        T[name] = table(["i", "j"], v)
+    for m in range(ns):
+        T[f"P{m:02d}"] = table(["i"], tabs.B[:, m])
+        for a in range(3):
+            T[f"Du{a}{m:02d}"] = table(["i"], tabs.D[a][:, m])
+        for cc in range(3):
+            T[f"u{cc}{m:02d}"] = table(["e"], coeffs[:, cc * ns + m])
+    nu, dt = cfg.consts
+    k["constants"] = {"nu": nu, "dt": dt}
+    st = k["statements"]
+    st.append(stmt(1, "rdt", ["/", 1.0, "dt"]))
+    for c in range(3):
+        st.append(stmt(2, f"uq{c}", coef_sum([f"u{c}{m:02d}" for m in range(ns)],
+                                             [f"P{m:02d}" for m in range(ns)])))
+        for b in range(3):
+            st.append(stmt(2, f"gu{c}{b}", add(*[
+                mul(S(f"u{c}{m:02d}", "e"), add(*[mul(f"K{a}{b}", S(f"Du{a}{m:02d}", "i"))
+                                                 for a in range(3)])) for m in range(ns)])))
+    for c in range(3):
+        st.append(stmt(2, f"adv{c}", add(mul(f"uq{c}", "rdt"),
+                                         *[mul(f"uq{b}", f"gu{c}{b}") for b in range(3)])))
+
+    def g(c, b):
+        return grad(lambda a: f"Dv{c}{a}", "j", b)
+
+    terms = []
+    for c in range(3):
+        terms.append(mul(f"adv{c}", S(f"Bv{c}", "i", "j")))
+        terms.append(mul("nu", add(*[mul(f"gu{c}{b}", g(c, b)) for b in range(3)])))
+    rhs = mul(add(*terms), S("W", "i"), "adet")
+    st.append(stmt(3, ["r", "e", "j"], rhs, "+="))
+    return k
+
+
+VECTOR_FORMS = {
+    fe.HELMHOLTZ: ("b", helmholtz_load),
+    fe.HYPERELASTICITY: ("r", hyperelasticity_residual),
+    fe.BURGERS: ("r", burgers_residual),
+}
+
+
+def build_vector(cfg, coords, coeffs, tabs=None):
+    """Arity-1 kernel of a config's form family: (output_name, ir_dict)."""
+    tabs = tabs if tabs is not None else fe.tables(cfg)
+    if cfg.kind not in VECTOR_FORMS:
+        raise ValueError(f"no element-vector form for kind {cfg.kind}")
+    name, fn = VECTOR_FORMS[cfg.kind]
+    return name, fn(cfg, np.asarray(coords, dtype=np.float64),
+                    np.asarray(coeffs, dtype=np.float64), tabs)
+
+
 def build(cfg, coords, coeffs, tabs=None, encoding="ufl"):
     """IR kernel(s) for a config: a list of (output_name, ir_dict)."""
-    tabs = tabs or fe.tables(cfg)
+    tabs = tabs if tabs is not None else fe.tables(cfg)
     coords = np.asarray(coords, dtype=np.float64)
     coeffs = np.asarray(coeffs, dtype=np.float64)
     if cfg.kind == fe.HELMHOLTZ:
