@@ -143,7 +143,91 @@ class Emitted:
         return int(np.prod(self.shape(name, ncells), dtype=np.int64))
 
 
-def emit(ir: dict | str, fn: str = "femopt_kernel") -> Emitted:
+def _op_counts(tree, J, ext):
+    """Arithmetic nodes executed per cell outside / inside the row loops (J)."""
+    def ops(x):
+        if isinstance(x, list) and x and x[0] in ("+", "*", "/", "call"):
+            return max(1, len(x) - 2) + sum(ops(a) for a in x[1:])
+        if isinstance(x, list) and x and x[0] == "sym":
+            return 0
+        return 0
+
+    tot = [0, 0]
+
+    def walk(nodes, mult, inJ):
+        for n in nodes:
+            if n[0] == "loop":
+                _, idx, b, e, body, cls = n
+                if cls == "orderfree":
+                    walk(body, mult, inJ)
+                else:
+                    walk(body, mult * max(0, e - b), inJ or idx == J)
+            else:
+                tot[1 if inJ else 0] += mult * (1 + ops(n[4]))
+
+    walk(tree, 1, False)
+    return tot
+
+
+def _warp_plan(tree, outputs, dims, temps, e_index, ext):
+    """The warp-per-cell mapping, if the nest allows it: the output rows (first
+    linear index J) are spread over the lanes, every other loop runs in full on
+    each lane.  Returns J or None."""
+    if e_index is None:
+        return None
+    rows = {tuple(dims[o][:2]) for o in outputs}
+    if len(rows) != 1:
+        return None
+    (e0, J), = rows
+    if e0 != e_index or J is None:
+        return None
+    ok = True
+    written_in_J, read_outside_J = set(), set()
+
+    def names_in(x, acc):
+        if isinstance(x, str):
+            acc.add(x)
+        elif isinstance(x, list) and x:
+            if x[0] == "sym":
+                acc.add(x[1])
+            for a in x[1:]:
+                names_in(a, acc)
+
+    def walk(nodes, inJ):
+        nonlocal ok
+        for n in nodes:
+            if n[0] == "loop":
+                _, idx, b, e, body, _ = n
+                if idx == J:
+                    if inJ or b != 0 or e != ext[J]:
+                        ok = False
+                    walk(body, True)
+                else:
+                    walk(body, inJ)
+            else:
+                _, name, idx, op, rhs = n
+                used = set()
+                names_in(rhs, used)
+                if any(o in used for o in outputs):
+                    ok = False  # outputs are write-only in femopt nests
+                if name in outputs:
+                    if not inJ or op != "+=" or idx[:2] != [e_index, J]:
+                        ok = False
+                elif inJ:
+                    written_in_J.add(name)
+                if not inJ:
+                    read_outside_J.update(used)
+
+    walk(tree, False)
+    if not ok or (written_in_J & read_outside_J):
+        return None
+    return J
+
+
+def emit(ir: dict | str, fn: str = "femopt_kernel", strategy: str = "auto") -> Emitted:
+    """Generate the kernel.  ``strategy``: "thread" (one thread per cell), "warp"
+    (one warp per cell, output rows over the lanes, accumulators in registers),
+    or "auto" (warp when the nest allows it and the output has >= 8 rows)."""
     if isinstance(ir, str):
         ir = json.loads(ir)
     ext = {k: int(v) for k, v in ir["indices"].items()}
@@ -190,6 +274,23 @@ def emit(ir: dict | str, fn: str = "femopt_kernel") -> Emitted:
     for o in outputs:
         if o not in dims:
             raise IRError(f"output {o} is never written")
+
+    J = _warp_plan(tree, outputs, dims, temps, e_index, ext)
+    if strategy == "auto":
+        strategy = "thread"
+        if J is not None and ext[J] >= 8:
+            o_out, o_in = _op_counts(tree, J, ext)
+            # the warp mapping repeats the out-of-row work on every lane
+            if 31 * o_out < 0.25 * o_in:
+                strategy = "warp"
+    if strategy == "warp" and J is None:
+        raise IRError("the warp mapping does not apply to this nest")
+    if strategy not in ("thread", "warp"):
+        raise IRError(f"unknown strategy {strategy!r}")
+    warp = strategy == "warp"
+    acc_dims = {d for o in outputs for d in dims[o][2:]}
+    R = (ext[J] + 31) // 32 if warp else 0
+    rest = {o: int(np.prod([ext[d] for d in dims[o][2:]], dtype=np.int64)) for o in outputs}
 
     inputs = sorted(n for n, t in tables.items() if t.get("provenance", "input") != "preevaluated")
     preev = sorted(n for n, t in tables.items() if t.get("provenance", "input") == "preevaluated")
@@ -267,12 +368,29 @@ def emit(ir: dict | str, fn: str = "femopt_kernel") -> Emitted:
                 _, idx, b, e, body, _ = n
                 if idx == e_index:
                     raise IRError("nested element loop")
+                if warp and idx == J:  # this lane's rows: J = lane + 32 r
+                    lines.append(f"{pad}#pragma unroll")
+                    lines.append(f"{pad}for (int r_ = 0; r_ < {R}; ++r_) {{")
+                    lines.append(f"{pad}  const int i_{_ident(J)} = lane_ + 32 * r_;")
+                    lines.append(f"{pad}  if (i_{J} < {e}) {{")
+                    emit_nodes(body, ind + 2)
+                    lines.append(f"{pad}  }}")
+                    lines.append(f"{pad}}}")
+                    continue
+                if warp and e - b <= 64 and idx in acc_dims and \
+                        (e - b) * _op_counts(body, None, ext)[0] <= 4096:
+                    lines.append(f"{pad}#pragma unroll")  # accumulators stay in registers
                 lines.append(f"{pad}for (int i_{_ident(idx)} = {b}; i_{idx} < {e}; ++i_{idx}) {{")
                 emit_nodes(body, ind + 1)
                 lines.append(f"{pad}}}")
             else:
                 _, name, idx, op, rhs = n
-                if name in outputs:
+                if name in outputs and warp:
+                    flat = "0"
+                    for d, i in zip(dims[name][2:], idx[2:]):
+                        flat = f"({flat} * {ext[d]} + i_{i})"
+                    target = f"a_{name}[r_ * {rest[name]} + {flat}]"
+                elif name in outputs:
                     target = f"o_{name}[{offset(name, idx)}]"
                 elif temps[name]:
                     flat = "0"
@@ -297,12 +415,30 @@ def emit(ir: dict | str, fn: str = "femopt_kernel") -> Emitted:
     if any(n[0] == "stmt" and n[1] in outputs for n in pre):
         raise IRError("output written outside the element loop")
     emit_nodes(pre, 1)
-    if e_index is not None:
+    if warp:
+        lines.append(f"  const long i_{e_index} = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;")
+        lines.append("  const int lane_ = threadIdx.x & 31;")
+        lines.append(f"  if (i_{e_index} >= E) return;")
+        for o in outputs:
+            lines.append(f"  double a_{o}[{R * rest[o]}];")
+            lines.append("  #pragma unroll")
+            lines.append(f"  for (int x_ = 0; x_ < {R * rest[o]}; ++x_) a_{o}[x_] = 0.0;")
+    elif e_index is not None:
         lines.append(f"  const long i_{e_index} = (long)blockIdx.x * blockDim.x + threadIdx.x;")
         lines.append(f"  if (i_{e_index} >= E) return;")
     else:
         lines.append("  if (blockIdx.x != 0 || threadIdx.x != 0) return;")
     emit_nodes(body, 1)
+    if warp:  # the output += contract: one add per entry, rows contiguous
+        for o in outputs:
+            lines.append("  #pragma unroll")
+            lines.append(f"  for (int r_ = 0; r_ < {R}; ++r_) {{")
+            lines.append(f"    const long row_ = lane_ + 32 * r_;")
+            lines.append(f"    if (row_ < {ext[J]}) {{")
+            lines.append(f"      double* dst_ = o_{o} + (i_{e_index} * {ext[J]} + row_) * {rest[o]};")
+            lines.append(f"      for (int x_ = 0; x_ < {rest[o]}; ++x_) dst_[x_] += a_{o}[r_ * {rest[o]} + x_];")
+            lines.append("    }")
+            lines.append("  }")
 
     decl = []
     for name in sorted(temps):
@@ -330,7 +466,9 @@ def emit(ir: dict | str, fn: str = "femopt_kernel") -> Emitted:
     src += decl
     src += lines
     src.append("}")
-    return Emitted("\n".join(src) + "\n", fn, outputs, inputs, cnames, preev, e_index, ext, dims)
+    em = Emitted("\n".join(src) + "\n", fn, outputs, inputs, cnames, preev, e_index, ext, dims)
+    em.strategy = strategy
+    return em
 
 
 # ----------------------------------------------------------------------------
@@ -368,8 +506,8 @@ class IRKernel:
 
     BLOCK = 128
 
-    def __init__(self, ir: dict | str, fn: str = "femopt_kernel"):
-        self.em = emit(ir, fn)
+    def __init__(self, ir: dict | str, fn: str = "femopt_kernel", strategy: str = "auto"):
+        self.em = emit(ir, fn, strategy)
         self.cubin = compile_cubin(self.em.source, fn + ".cu")
         self._func = None
 
@@ -424,7 +562,7 @@ class IRKernel:
             types.append(ctypes.c_double)
         vals.append(int(ncells))
         types.append(ctypes.c_long)
-        n_threads = ncells if em.e_index is not None else 1
+        n_threads = (ncells * (32 if em.strategy == "warp" else 1)) if em.e_index is not None else 1
         grid = max(1, (n_threads + self.BLOCK - 1) // self.BLOCK)
         s = torch.cuda.current_stream().cuda_stream if stream is None else (
             stream if isinstance(stream, int) else stream.cuda_stream)

@@ -65,12 +65,30 @@ def test_bad_ir_is_rejected():
 # ----------------------------------------------------------------------------
 # on the GPU
 # ----------------------------------------------------------------------------
+def _strategies(case):
+    js, _, _ = load(case)
+    out = ["thread"]
+    try:
+        emit_cuda.emit(js, strategy="warp")
+        out.append("warp")
+    except emit_cuda.IRError:
+        pass
+    return out
+
+
+STRATS = [(c, s) for c in CASES for s in _strategies(c)]
+
+
+def test_warp_mapping_applies_to_the_larger_nests():
+    assert sum(s == "warp" for _, s in STRATS) >= 8
+
+
 @pytest.mark.gpu
-@pytest.mark.parametrize("case", CASES)
-def test_matches_femopt_emitted_c(case):
+@pytest.mark.parametrize("case,strategy", STRATS)
+def test_matches_femopt_emitted_c(case, strategy):
     pytest.importorskip("torch")
     js, d, z = load(case)
-    K = emit_cuda.IRKernel(js)
+    K = emit_cuda.IRKernel(js, strategy=strategy)
     got = K.run_ir_tables(d)
     for o in d["outputs"]:
         ref_c = z[f"emitc_{o}"].reshape(-1)
@@ -78,7 +96,8 @@ def test_matches_femopt_emitted_c(case):
         g = got[o].reshape(-1)
         scale = np.abs(ref_i).max()
         assert np.abs(g - ref_i).max() <= 1e-13 * scale
-        assert np.array_equal(g, ref_c), f"{case}/{o}: not bit-identical to femopt's emitted C"
+        assert np.array_equal(g, ref_c), \
+            f"{case}/{o} ({strategy}): not bit-identical to femopt's emitted C"
 
 
 @pytest.mark.gpu
