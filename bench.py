@@ -135,6 +135,8 @@ def load_peaks():
     # this pool's B200 (tools/fp64_peak.cu -> profiles/fp64_peak_r01.txt).
     peaks["fp64_tflops"] = 37.0
     peaks["fp64_source"] = "measured DMMA peak, profiles/fp64_peak_r01.txt"
+    peaks["dfma_tflops"] = 33.9
+    peaks["dfma_source"] = "measured DFMA peak, profiles/fp64_peak_r01.txt"
     return peaks
 
 
@@ -157,6 +159,20 @@ def profile_traffic(cfg_name):
         return d.get(cfg_name, {}).get("dram_bytes_per_launch")
     except (OSError, ValueError):
         return None
+
+
+def uses_dmma(cfg_name, kernel_name):
+    """Whether the committed ncu capture of this kernel executed DMMA instructions
+    (None if unknown): a DFMA-only kernel's FP64 ceiling is the DFMA peak."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            d = json.load(f).get(cfg_name, {})
+    except (OSError, ValueError):
+        return None
+    if ncu_flops(cfg_name, kernel_name) is None:
+        return None
+    b = d.get("fp64_flops_ncu_breakdown", {})
+    return b.get("sm__ops_path_tensor_src_fp64", 0) > 0
 
 
 def ncu_flops(cfg_name, kernel_name):
@@ -348,6 +364,10 @@ def run_ours(args, rank, world, local):
     avg_launch_s = (sum(per_launch) / len(per_launch)) / 1e3
     # the bound is whichever floor is longer: algorithmic bytes at the measured HBM
     # bandwidth or algorithmic flops at the measured FP64 (DMMA) peak
+    # FP64 ceiling of the pipe the kernel runs on: DMMA (tensor) or, for a
+    # DFMA-only kernel, the DFMA peak (they share one datapath, tools/fp64_mix.cu)
+    if uses_dmma(args.config, form.info["kernel_name"]) is False:
+        peaks["fp64_tflops"], peaks["fp64_source"] = peaks["dfma_tflops"], peaks["dfma_source"]
     hbm_bound = bpc / peaks["hbm_gbs"] >= F_roof / (peaks["fp64_tflops"] * 1e3)
     if hbm_bound:
         achieved = E * bpc / avg_launch_s / 1e9
@@ -355,7 +375,8 @@ def run_ours(args, rank, world, local):
                 "frac": achieved / peaks["hbm_gbs"], "peak_source": peaks["hbm_source"]}
     else:
         achieved = E * F_roof / avg_launch_s / 1e12
-        roof = {"bound": "tensor", "pipe": "fp64 (DMMA/DFMA)", "achieved": achieved,
+        roof = {"bound": "tensor", "pipe": "fp64 " + ("DFMA" if "DFMA" in peaks["fp64_source"] else "DMMA"),
+                "achieved": achieved,
                 "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
                 "frac": achieved / peaks["fp64_tflops"], "peak_source": peaks["fp64_source"]}
     tr = profile_traffic(args.config)
