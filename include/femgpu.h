@@ -141,6 +141,30 @@ int femgpu_kernel_argv(const femgpu_form* f, long ncells, double* const* o,
 int femgpu_kernel_argc(const femgpu_form* f, int group, int* count);
 int femgpu_kernel_argname(const femgpu_form* f, int group, int index, char* buf, size_t len);
 
+/* ---------------------------------------------------------------------------
+ * Either side of the path (the reference reads
+ * pre-gathered per-cell tables, proj/tests/kernels.hpp:186-188, and stops at
+ * the element matrix).  All pointers are device pointers.
+ * ------------------------------------------------------------------------- */
+
+/* Gather the per-cell inputs of femgpu_assemble from global vectors:
+ * coords[e][v][c] = V[cells[e][v]][c]  (cells: [ncells][4] vertex ids),
+ * coeffs[e][s]    = coef[coef_idx[e][s]] (coef_idx: [ncells][ncoef]). */
+int femgpu_gather(long ncells, int ncoef, const double* V, const int* cells, const double* coef,
+                  const int* coef_idx, double* coords, double* coeffs, void* stream);
+
+/* Symbolic assembly: pos[e][j][k] = position of column dof_map[e][k] in row
+ * dof_map[e][j] of the CSR pattern (row_ptr [nrows+1], col_idx sorted per row).
+ * Synchronizes the stream; FEMGPU_ERR_INCONSISTENT_LAYOUT if any entry of an
+ * element matrix is outside the pattern. */
+int femgpu_csr_positions(long ncells, int n, const int* dof_map, const long* row_ptr,
+                         const int* col_idx, long* pos, void* stream);
+
+/* Numeric assembly: vals[pos[i]] += A[i] for i < nentries (FP64 atomics;
+ * A = the element matrices [ncells][n][n] of femgpu_assemble). */
+int femgpu_scatter_add(long nentries, const double* A, const long* pos, double* vals,
+                       void* stream);
+
 /* Message for the most recent failure on this thread ("" if none). */
 const char* femgpu_last_error(void);
 

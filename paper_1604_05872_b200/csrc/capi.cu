@@ -576,6 +576,54 @@ int femgpu_kernel_argv(const femgpu_form* f, long ncells, double* const* o, cons
   });
 }
 
+int femgpu_gather(long ncells, int ncoef, const double* V, const int* cells, const double* coef,
+                  const int* coef_idx, double* coords, double* coeffs, void* stream) {
+  return guarded([&] {
+    if (ncells < 0 || ncoef < 0) throw Error(FEMGPU_ERR_INVALID_ARG, "negative size");
+    if (ncells == 0) return;
+    if (!V || !cells || !coords || (ncoef > 0 && (!coef || !coef_idx || !coeffs)))
+      throw Error(FEMGPU_ERR_INVALID_ARG, "null buffer");
+    cuda_check(femgpu::launch_gather(ncells, ncoef, V, cells, coef, coef_idx, coords, coeffs,
+                                     static_cast<cudaStream_t>(stream)),
+               "gather_kernel");
+  });
+}
+
+int femgpu_csr_positions(long ncells, int n, const int* dof_map, const long* row_ptr,
+                         const int* col_idx, long* pos, void* stream) {
+  return guarded([&] {
+    if (ncells < 0 || n <= 0) throw Error(FEMGPU_ERR_INVALID_ARG, "bad size");
+    if (ncells == 0) return;
+    if (!dof_map || !row_ptr || !col_idx || !pos) throw Error(FEMGPU_ERR_INVALID_ARG, "null buffer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int* d_missing = nullptr;
+    cuda_check(cudaMallocAsync(&d_missing, sizeof(int), s), "cudaMallocAsync");
+    cuda_check(cudaMemsetAsync(d_missing, 0, sizeof(int), s), "cudaMemsetAsync");
+    cudaError_t e = femgpu::launch_csr_positions(ncells, n, dof_map, row_ptr, col_idx, pos,
+                                                 d_missing, s);
+    int missing = 0;
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(&missing, d_missing, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFreeAsync(d_missing, s);
+    cuda_check(e, "csr_positions_kernel");
+    if (missing)
+      throw Error(FEMGPU_ERR_INCONSISTENT_LAYOUT,
+                  std::to_string(missing) + " element-matrix entries outside the CSR pattern");
+  });
+}
+
+int femgpu_scatter_add(long nentries, const double* A, const long* pos, double* vals,
+                       void* stream) {
+  return guarded([&] {
+    if (nentries < 0) throw Error(FEMGPU_ERR_INVALID_ARG, "negative size");
+    if (nentries == 0) return;
+    if (!A || !pos || !vals) throw Error(FEMGPU_ERR_INVALID_ARG, "null buffer");
+    cuda_check(femgpu::launch_scatter_add(nentries, A, pos, vals, static_cast<cudaStream_t>(stream)),
+               "scatter_add_kernel");
+  });
+}
+
 const char* femgpu_last_error(void) { return g_last_error.c_str(); }
 
 const char* femgpu_version(void) { return "femgpu 0.1 (sm_100a, FP64)"; }

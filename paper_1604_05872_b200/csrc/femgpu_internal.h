@@ -39,6 +39,14 @@ void elas_tensor_tables(int nq, const double* W, const double* D, const double* 
 cudaError_t launch_elas_tensor(long E, const double* coords, const double* coef, const double* tab,
                                double* A, int acc, cudaStream_t s);
 
+// Gather / symbolic / numeric global assembly (see global.cu).
+cudaError_t launch_gather(long E, int ncoef, const double* V, const int* cells, const double* coef,
+                          const int* coef_idx, double* coords, double* coeffs, cudaStream_t s);
+cudaError_t launch_csr_positions(long E, int n, const int* dof, const long* row_ptr,
+                                 const int* col_idx, long* pos, int* missing, cudaStream_t s);
+cudaError_t launch_scatter_add(long total, const double* A, const long* pos, double* vals,
+                               cudaStream_t s);
+
 // Burgers tensor schedule (see burgers.cu).
 bool burgers_supported(int nq, int ns);
 size_t burgers_table_doubles();

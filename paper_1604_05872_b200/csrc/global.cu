@@ -1,0 +1,111 @@
+// global.cu -- the steps either side of the path:
+// gather of per-cell inputs from global vectors before it, scatter-add of the
+// element matrices into a global CSR matrix after it.
+//
+// The reference stops at the element matrix and reads pre-gathered
+// per-cell tables (proj/tests/kernels.hpp:186-188); a FEM code around it
+// performs these two steps.  Both are HBM/latency-bound integer-indexed
+// streams, so they are written as such (no tensor cores): grid-stride over the
+// output index space with coalesced stores (gather) and coalesced loads +
+// FP64 atomics (scatter).  The CSR positions of a cell's n x n entries depend
+// only on the mesh, so they are resolved once (binary search in the sorted
+// row) and reused by every assembly -- the usual split between symbolic and
+// numeric assembly.
+#include <cstdint>
+
+#include "common.cuh"
+#include "femgpu_internal.h"
+
+namespace femgpu {
+
+namespace {
+
+__global__ void gather_kernel(long E, int ncoef, const double* __restrict__ V,
+                              const int* __restrict__ cells, const double* __restrict__ coef,
+                              const int* __restrict__ coef_idx, double* __restrict__ coords,
+                              double* __restrict__ coeffs) {
+  const long nx = E * 12, total = nx + E * (long)ncoef;
+  for (long t = (long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long)gridDim.x * blockDim.x) {
+    if (t < nx) {  // coords[e][v][c] = V[cells[e][v]][c]
+      const long e = t / 12;
+      const int r = (int)(t - e * 12), v = r / 3, c = r - 3 * v;
+      coords[t] = __ldg(&V[(long)__ldg(&cells[e * 4 + v]) * 3 + c]);
+    } else {  // coeffs[e][s] = coef[coef_idx[e][s]]
+      const long u = t - nx;
+      coeffs[u] = __ldg(&coef[__ldg(&coef_idx[u])]);
+    }
+  }
+}
+
+// pos[e][j][k] = index of column dof[e][k] in row dof[e][j] (-1 if absent)
+__global__ void csr_positions_kernel(long E, int n, const int* __restrict__ dof,
+                                     const long* __restrict__ row_ptr,
+                                     const int* __restrict__ col_idx, long* __restrict__ pos,
+                                     int* __restrict__ missing) {
+  const long rows = E * (long)n;
+  for (long t = (long)blockIdx.x * blockDim.x + threadIdx.x; t < rows;
+       t += (long)gridDim.x * blockDim.x) {
+    const long e = t / n;
+    const int r = __ldg(&dof[t]);
+    const long b = __ldg(&row_ptr[r]), len = __ldg(&row_ptr[r + 1]) - b;
+    const int* cols = col_idx + b;
+    long* out = pos + t * n;
+    for (int k = 0; k < n; ++k) {
+      const int c = __ldg(&dof[e * n + k]);
+      long lo = 0, hi = len;  // first column >= c
+      while (lo < hi) {
+        const long mid = (lo + hi) >> 1;
+        if (__ldg(&cols[mid]) < c) lo = mid + 1; else hi = mid;
+      }
+      if (lo < len && __ldg(&cols[lo]) == c) {
+        out[k] = b + lo;
+      } else {
+        out[k] = -1;
+        atomicAdd(missing, 1);
+      }
+    }
+  }
+}
+
+__global__ void scatter_add_kernel(long total, const double* __restrict__ A,
+                                   const long* __restrict__ pos, double* __restrict__ vals) {
+  for (long t = (long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long)gridDim.x * blockDim.x) {
+    const long p = __ldg(&pos[t]);
+    if (p >= 0) atomicAdd(&vals[p], __ldg(&A[t]));
+  }
+}
+
+int grid_for(long work, int block) {
+  const long want = (work + block - 1) / block;
+  const long cap = 8L * kNumSMs * (2048 / block);
+  return (int)(want < cap ? (want > 0 ? want : 1) : cap);
+}
+
+}  // namespace
+
+cudaError_t launch_gather(long E, int ncoef, const double* V, const int* cells, const double* coef,
+                          const int* coef_idx, double* coords, double* coeffs, cudaStream_t s) {
+  if (E <= 0) return cudaSuccess;
+  gather_kernel<<<grid_for(E * (12 + ncoef), 256), 256, 0, s>>>(E, ncoef, V, cells, coef, coef_idx,
+                                                               coords, coeffs);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_csr_positions(long E, int n, const int* dof, const long* row_ptr,
+                                 const int* col_idx, long* pos, int* missing, cudaStream_t s) {
+  if (E <= 0) return cudaSuccess;
+  csr_positions_kernel<<<grid_for(E * n, 128), 128, 0, s>>>(E, n, dof, row_ptr, col_idx, pos,
+                                                            missing);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter_add(long total, const double* A, const long* pos, double* vals,
+                               cudaStream_t s) {
+  if (total <= 0) return cudaSuccess;
+  scatter_add_kernel<<<grid_for(total, 256), 256, 0, s>>>(total, A, pos, vals);
+  return cudaGetLastError();
+}
+
+}  // namespace femgpu

@@ -170,6 +170,13 @@ def cube_mesh(N: int, seed: int = 1604, jitter: float = 0.1) -> np.ndarray:
     drawn from PCG64(seed) in vertex order; boundary vertices stay put.  Cells
     are ordered hex-major (x fastest), the 6 tets of a hex consecutive.
     """
+    V, cells = cube_topology(N, seed, jitter)
+    return np.ascontiguousarray(V[cells])
+
+
+def cube_topology(N: int, seed: int = 1604, jitter: float = 0.1):
+    """The mesh of ``cube_mesh`` as vertices V [nv][3] and cells [E][4] (vertex ids,
+    id = (k (N+1) + j)(N+1) + i for lattice point (i, j, k))."""
     h = 1.0 / N
     g = np.arange(N + 1, dtype=np.float64) * h
     zz, yy, xx = np.meshgrid(g, g, g, indexing="ij")
@@ -195,7 +202,7 @@ def cube_mesh(N: int, seed: int = 1604, jitter: float = 0.1) -> np.ndarray:
             off[perm[s]] += 1
             cells[:, t, s + 1] = vid(hi + off[0], hj + off[1], hk + off[2])
     cells = cells.reshape(-1, 4)
-    return np.ascontiguousarray(V[cells])
+    return V, cells
 
 
 def draw_dofs(E: int, ndof: int, lo: float, hi: float, seed: int) -> np.ndarray:

@@ -40,7 +40,8 @@ ERROR_NAMES = {
 # Every symbol include/femgpu.h declares (checked by tests/test_abi.py).
 EXPORTS = ("femgpu_form_create", "femgpu_form_free", "femgpu_form_get_info", "femgpu_assemble",
            "femgpu_assemble_host", "femgpu_kernel_argv", "femgpu_kernel_argc",
-           "femgpu_kernel_argname", "femgpu_last_error", "femgpu_version")
+           "femgpu_kernel_argname", "femgpu_gather", "femgpu_csr_positions",
+           "femgpu_scatter_add", "femgpu_last_error", "femgpu_version")
 
 
 class FemgpuError(RuntimeError):
@@ -88,6 +89,9 @@ def lib():
         L.femgpu_kernel_argname.argtypes = [vp, C.c_int, C.c_int, C.c_char_p, C.c_size_t]
         L.femgpu_last_error.restype = C.c_char_p
         L.femgpu_version.restype = C.c_char_p
+        L.femgpu_gather.argtypes = [C.c_long, C.c_int, vp, vp, vp, vp, vp, vp, vp]
+        L.femgpu_csr_positions.argtypes = [C.c_long, C.c_int, vp, vp, vp, vp, vp]
+        L.femgpu_scatter_add.argtypes = [C.c_long, vp, vp, vp, vp]
         _lib = L
     return _lib
 
@@ -210,3 +214,32 @@ class Form:
 
 def version() -> str:
     return lib().femgpu_version().decode()
+
+
+# ----------------------------------------------------------------------------
+# either side of the path: gather, symbolic and numeric global assembly
+# (device tensors; see include/femgpu.h and mesh.py)
+# ----------------------------------------------------------------------------
+def _stream(stream):
+    return None if stream is None else (stream if isinstance(stream, int) else stream.cuda_stream)
+
+
+def gather(V, cells, coef, coef_idx, coords, coeffs, stream=None):
+    """coords[e] = V[cells[e]], coeffs[e][s] = coef[coef_idx[e][s]] (int32 index maps)."""
+    E, ncoef = int(cells.shape[0]), int(coef_idx.shape[1]) if coef_idx is not None else 0
+    _check(lib().femgpu_gather(E, ncoef, _devptr(V), _devptr(cells), _devptr(coef),
+                               _devptr(coef_idx), _devptr(coords), _devptr(coeffs),
+                               _stream(stream)))
+
+
+def csr_positions(dof_map, row_ptr, col_idx, pos, stream=None):
+    """pos[e][j][k] = CSR position of (dof_map[e][j], dof_map[e][k]) (synchronizes)."""
+    E, n = int(dof_map.shape[0]), int(dof_map.shape[1])
+    _check(lib().femgpu_csr_positions(E, n, _devptr(dof_map), _devptr(row_ptr), _devptr(col_idx),
+                                      _devptr(pos), _stream(stream)))
+
+
+def scatter_add(A, pos, vals, stream=None):
+    """vals[pos[i]] += A[i] over all element-matrix entries."""
+    _check(lib().femgpu_scatter_add(int(A.numel()), _devptr(A), _devptr(pos), _devptr(vals),
+                                    _stream(stream)))
