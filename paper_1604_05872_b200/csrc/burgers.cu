@@ -54,7 +54,7 @@ constexpr int NBU = 15;            // upper 4x4 blocks (J <= K) of the 20x20 (j,
 constexpr int KS1 = 3;             // GEMM-1 k4 steps over the derivative space
 constexpr int RMAX = 4 * KS1;      // largest supported derivative-space rank
 constexpr int DNR = 16;            // Dn rows held in smem (two n8 tiles, zero past rank)
-constexpr int KS2 = 18;            // GEMM-2 k4 steps: 60 (n,a) + 6 (G) + 1 (mass) + pad
+constexpr int KS2 = 17;            // GEMM-2 k4 steps: 60 (n,a) + 6 (G) + 1 (mass) + 1 pad
 constexpr int CELLS = 16;
 constexpr int WARPS = 16;
 constexpr int THREADS = 32 * WARPS;
