@@ -165,6 +165,44 @@ int femgpu_csr_positions(long ncells, int n, const int* dof_map, const long* row
 int femgpu_scatter_add(long nentries, const double* A, const long* pos, double* vals,
                        void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Any femopt kernel: the GPU counterpart of femopt's
+ * emit_c backend (proj/src/emit_c.cpp:108-174).  femgpu_ir_create takes the
+ * kernel IR JSON (proj/README.md:68-100, raw or as femopt_kernel_to_json writes
+ * it), generates CUDA for it and compiles it with NVRTC for sm_100a.  Argument
+ * groups and order are emit_c's: outputs, input tables, constants, each sorted
+ * by name (emit_c.cpp:137-140); outputs are accumulated with +=; results are
+ * bit-identical to femopt's emitted C compiled with -ffp-contract=off.
+ * ------------------------------------------------------------------------- */
+typedef struct femgpu_ir femgpu_ir;
+
+enum { FEMGPU_IR_AUTO = 0, FEMGPU_IR_THREAD_PER_CELL = 1, FEMGPU_IR_WARP_PER_CELL = 2 };
+
+typedef struct {
+  int noutputs, ninputs, nconstants;
+  int per_cell;  /* 1: the nest has an order-free element loop (ncells applies) */
+  int strategy;  /* FEMGPU_IR_THREAD_PER_CELL or FEMGPU_IR_WARP_PER_CELL */
+} femgpu_ir_info;
+
+/* Parse, generate and compile (FEMGPU_ERR_NOT_FEM_NEST for an IR it cannot
+ * emit, FEMGPU_ERR_CUDA if NVRTC is missing or rejects the source). */
+int femgpu_ir_create(const char* ir_json, int strategy, femgpu_ir** out);
+void femgpu_ir_free(femgpu_ir* k);
+int femgpu_ir_get_info(const femgpu_ir* k, femgpu_ir_info* info);
+/* Names (group 0 outputs, 1 input tables, 2 constants) and element counts
+ * (group 0/1) of the arguments for ncells cells. */
+int femgpu_ir_argname(const femgpu_ir* k, int group, int index, char* buf, size_t len);
+int femgpu_ir_arg_size(const femgpu_ir* k, int group, int index, long ncells, long* size);
+/* The generated CUDA source. */
+const char* femgpu_ir_source(const femgpu_ir* k);
+/* Device pointers, emit_c order; outputs += ; ncells replaces the IR's extent
+ * of the element index. */
+int femgpu_ir_launch(femgpu_ir* k, long ncells, double* const* outputs,
+                     const double* const* inputs, const double* constants, void* stream);
+/* Host pointers, emit_c's calling convention (synchronous). */
+int femgpu_ir_argv(femgpu_ir* k, long ncells, double* const* o, const double* const* t,
+                   const double* c);
+
 /* Message for the most recent failure on this thread ("" if none). */
 const char* femgpu_last_error(void);
 

@@ -312,6 +312,10 @@ void launch(const femgpu_form* f, long E, const double* coords, const double* co
 
 }  // namespace
 
+namespace femgpu {
+void set_last_error(const std::string& m) { g_last_error = m; }
+}  // namespace femgpu
+
 extern "C" {
 
 int femgpu_form_create(const femgpu_form_desc* d, femgpu_form** out) {

@@ -4,7 +4,12 @@
 #include <cuda_runtime.h>
 #include <stddef.h>
 
+#include <string>
+
 namespace femgpu {
+
+// The thread-local message femgpu_last_error() returns (capi.cu).
+void set_last_error(const std::string& message);
 
 // Pre-evaluated P1 Helmholtz tables (kernel parameters: constant bank).
 struct HelmP1Params {

@@ -1,0 +1,913 @@
+// ir_backend.cpp -- femopt kernel IR -> sm_100a kernel, behind the C ABI
+// (the GPU counterpart of the reference's only backend,
+// emit_c, /root/reference/proj/src/emit_c.cpp:108-174).
+//
+// femgpu_ir_create parses a femopt kernel IR (the JSON of proj/README.md:68-100:
+// flat statements with levels, or the nested body femopt's to_json writes),
+// generates CUDA C for it and compiles it with NVRTC for sm_100a; launches go
+// through the CUDA runtime's library API.  The generated code:
+//
+//   * maps the order-free element loop onto the grid -- one thread per cell, or
+//     one warp per cell with the output rows spread over the lanes and
+//     accumulated in registers (chosen by an op-count model; both exact);
+//   * prints every expression exactly as emit_c prints it (precedence-driven,
+//     nested sums and products flattened, emit_c.cpp:47-80) and is compiled
+//     with --fmad=false, so it performs femopt's emitted arithmetic operation
+//     for operation: results are bit-identical to femopt's emitted C compiled
+//     with -ffp-contract=off (tests/test_emit_cuda.py, golden IRs made by the
+//     reference itself);
+//   * keeps emit_c's calling convention: outputs, input tables, constants,
+//     each group sorted by name (emit_c.cpp:137-140); pre-evaluated tables are
+//     baked into the module; outputs are accumulated with += (:91-92,129).
+//
+// NVRTC is loaded with dlopen on first use, so libfemgpu does not depend on it
+// unless this backend is used.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/femgpu.h"
+#include "femgpu_internal.h"
+
+namespace irgen {
+
+struct IRError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// ----------------------------------------------------------------------------
+// minimal JSON
+// ----------------------------------------------------------------------------
+struct Json {
+  enum Kind { Null, Bool, Num, Str, Arr, Obj } kind = Null;
+  bool b = false;
+  double num = 0;
+  std::string str;
+  std::vector<Json> arr;
+  std::vector<std::pair<std::string, Json>> obj;
+
+  const Json* get(const std::string& k) const {
+    for (const auto& kv : obj)
+      if (kv.first == k) return &kv.second;
+    return nullptr;
+  }
+  const Json& at(const std::string& k) const {
+    const Json* j = get(k);
+    if (!j) throw IRError("IR: missing key '" + k + "'");
+    return *j;
+  }
+};
+
+struct Parser {
+  const char* p;
+  const char* end;
+  void ws() {
+    while (p < end && (*p == ' ' || *p == '\n' || *p == '\t' || *p == '\r')) ++p;
+  }
+  [[noreturn]] void fail(const char* what) { throw IRError(std::string("IR JSON: ") + what); }
+  Json value() {
+    ws();
+    if (p >= end) fail("unexpected end");
+    Json j;
+    const char c = *p;
+    if (c == '{') {
+      ++p;
+      j.kind = Json::Obj;
+      ws();
+      if (p < end && *p == '}') { ++p; return j; }
+      for (;;) {
+        ws();
+        Json k = value();
+        if (k.kind != Json::Str) fail("object key");
+        ws();
+        if (p >= end || *p != ':') fail("':'");
+        ++p;
+        j.obj.emplace_back(k.str, value());
+        ws();
+        if (p < end && *p == ',') { ++p; continue; }
+        if (p < end && *p == '}') { ++p; return j; }
+        fail("',' or '}'");
+      }
+    }
+    if (c == '[') {
+      ++p;
+      j.kind = Json::Arr;
+      ws();
+      if (p < end && *p == ']') { ++p; return j; }
+      for (;;) {
+        j.arr.push_back(value());
+        ws();
+        if (p < end && *p == ',') { ++p; continue; }
+        if (p < end && *p == ']') { ++p; return j; }
+        fail("',' or ']'");
+      }
+    }
+    if (c == '"') {
+      ++p;
+      j.kind = Json::Str;
+      while (p < end && *p != '"') {
+        if (*p == '\\') {
+          ++p;
+          if (p >= end) fail("escape");
+          const char e = *p;
+          j.str += e == 'n' ? '\n' : e == 't' ? '\t' : e;
+        } else {
+          j.str += *p;
+        }
+        ++p;
+      }
+      if (p >= end) fail("unterminated string");
+      ++p;
+      return j;
+    }
+    if (!strncmp(p, "true", 4)) { p += 4; j.kind = Json::Bool; j.b = true; return j; }
+    if (!strncmp(p, "false", 5)) { p += 5; j.kind = Json::Bool; return j; }
+    if (!strncmp(p, "null", 4)) { p += 4; return j; }
+    char* q = nullptr;
+    j.num = strtod(p, &q);
+    if (q == p) fail("value");
+    p = q;
+    j.kind = Json::Num;
+    return j;
+  }
+};
+
+Json parse(const char* text) {
+  Parser ps{text, text + strlen(text)};
+  Json j = ps.value();
+  ps.ws();
+  if (ps.p != ps.end) ps.fail("trailing characters");
+  return j;
+}
+
+// ----------------------------------------------------------------------------
+// IR tree
+// ----------------------------------------------------------------------------
+struct Node {
+  bool loop = false;
+  std::string index, cls, name, op;  // loop: index/cls; stmt: name/op
+  long begin = 0, end = 0;
+  std::vector<Node> body;
+  std::vector<std::string> idx;  // stmt lhs subscripts
+  const Json* rhs = nullptr;
+};
+
+[[noreturn]] void irfail(const std::string& m) { throw IRError("IR: " + m); }
+
+Node stmt_node(const Json& st) {
+  Node n;
+  const Json& lhs = st.at("lhs");
+  if (lhs.kind == Json::Str) {
+    n.name = lhs.str;
+  } else {
+    if (lhs.kind != Json::Arr || lhs.arr.empty()) irfail("bad lhs");
+    n.name = lhs.arr[0].str;
+    for (size_t i = 1; i < lhs.arr.size(); ++i) n.idx.push_back(lhs.arr[i].str);
+  }
+  const Json* op = st.get("op");
+  n.op = op ? op->str : "=";
+  n.rhs = &st.at("rhs");
+  return n;
+}
+
+std::vector<Node> from_nested(const Json& nodes, const std::map<std::string, long>& ext) {
+  std::vector<Node> out;
+  for (const Json& n : nodes.arr) {
+    const Json* L = n.get("loop");
+    if (!L && n.get("body") && n.get("index")) L = &n;
+    if (L) {
+      Node x;
+      x.loop = true;
+      x.index = L->at("index").str;
+      const Json* c = L->get("class");
+      if (c && c->kind == Json::Str) x.cls = c->str;
+      const Json* b = L->get("begin");
+      const Json* e = L->get("end");
+      x.begin = b ? (long)b->num : 0;
+      x.end = e ? (long)e->num : ext.at(x.index);
+      x.body = from_nested(L->at("body"), ext);
+      out.push_back(std::move(x));
+    } else {
+      out.push_back(stmt_node(n));
+    }
+  }
+  return out;
+}
+
+std::vector<Node> build_tree(const Json& ir, const std::map<std::string, long>& ext) {
+  if (ir.get("body")) return from_nested(ir.at("body"), ext);
+  std::vector<std::string> loops;
+  std::map<std::string, std::string> classes;
+  for (const Json& L : ir.at("loops").arr) {
+    loops.push_back(L.at("index").str);
+    const Json* c = L.get("class");
+    if (c && c->kind == Json::Str) classes[loops.back()] = c->str;
+  }
+  std::vector<Node> root;
+  std::vector<std::vector<Node>*> stack{&root};
+  for (const Json& st : ir.at("statements").arr) {
+    if (st.get("body") && st.get("index")) {
+      Json wrap;
+      wrap.kind = Json::Arr;
+      wrap.arr.push_back(st);
+      auto v = from_nested(wrap, ext);
+      stack.back()->push_back(std::move(v[0]));
+      continue;
+    }
+    const long level = (long)st.at("level").num;
+    if (level > (long)loops.size()) irfail("statement level exceeds the loop nest");
+    while ((long)stack.size() - 1 > level) stack.pop_back();
+    while ((long)stack.size() - 1 < level) {
+      Node x;
+      x.loop = true;
+      x.index = loops[stack.size() - 1];
+      x.cls = classes.count(x.index) ? classes[x.index] : "";
+      x.begin = 0;
+      x.end = ext.at(x.index);
+      stack.back()->push_back(std::move(x));
+      stack.push_back(&stack.back()->back().body);
+    }
+    stack.back()->push_back(stmt_node(st));
+  }
+  return root;
+}
+
+// ----------------------------------------------------------------------------
+// code generation
+// ----------------------------------------------------------------------------
+std::string lit(double x) {
+  char buf[64];
+  if (x == 0.0) return "0.0";
+  if (std::isfinite(x) && x == std::floor(x) && std::fabs(x) < 4503599627370496.0) {
+    snprintf(buf, sizeof buf, "%.1f", x);
+    return buf;
+  }
+  snprintf(buf, sizeof buf, "%a", x);
+  return buf;
+}
+
+bool ident_ok(const std::string& s) {
+  if (s.empty() || !(isalpha((unsigned char)s[0]) || s[0] == '_')) return false;
+  for (char c : s)
+    if (!(isalnum((unsigned char)c) || c == '_')) return false;
+  return true;
+}
+const std::string& ident(const std::string& s) {
+  if (!ident_ok(s)) irfail("bad name '" + s + "'");
+  return s;
+}
+
+const std::map<std::string, std::string>& calls() {
+  static const std::map<std::string, std::string> m = {
+      {"fabs", "fabs"}, {"sqrt", "sqrt"}, {"exp", "exp"},   {"log", "log"},   {"pow", "pow"},
+      {"sin", "sin"},   {"cos", "cos"},   {"tan", "tan"},   {"atan", "atan"}, {"atan2", "atan2"},
+      {"cbrt", "cbrt"}, {"fmin", "fmin"}, {"fmax", "fmax"}, {"abs", "fabs"}};
+  return m;
+}
+
+long ops(const Json& x) {
+  if (x.kind == Json::Arr && !x.arr.empty() && x.arr[0].kind == Json::Str) {
+    const std::string& op = x.arr[0].str;
+    if (op == "+" || op == "*" || op == "/" || op == "call") {
+      long s = std::max<long>(1, (long)x.arr.size() - 2);
+      for (size_t i = 1; i < x.arr.size(); ++i) s += ops(x.arr[i]);
+      return s;
+    }
+  }
+  return 0;
+}
+
+void op_counts(const std::vector<Node>& nodes, double mult, bool inJ, const std::string& J,
+               double tot[2]) {
+  for (const Node& n : nodes) {
+    if (n.loop) {
+      if (n.cls == "orderfree")
+        op_counts(n.body, mult, inJ, J, tot);
+      else
+        op_counts(n.body, mult * std::max<long>(0, n.end - n.begin), inJ || n.index == J, J, tot);
+    } else {
+      tot[inJ ? 1 : 0] += mult * (1 + ops(*n.rhs));
+    }
+  }
+}
+
+void names_in(const Json& x, std::set<std::string>& acc) {
+  if (x.kind == Json::Str) {
+    acc.insert(x.str);
+  } else if (x.kind == Json::Arr && !x.arr.empty()) {
+    if (x.arr[0].kind == Json::Str && x.arr[0].str == "sym" && x.arr.size() > 1)
+      acc.insert(x.arr[1].str);
+    for (size_t i = 1; i < x.arr.size(); ++i) names_in(x.arr[i], acc);
+  }
+}
+
+struct Emitter {
+  std::map<std::string, long> ext;
+  std::map<std::string, std::vector<std::string>> dims;   // tables and outputs
+  std::map<std::string, std::vector<std::string>> temps;
+  std::set<std::string> outs, tabs, consts;
+  std::string e_index, J;
+  bool warp = false;
+  long R = 0;
+  std::map<std::string, long> rest;
+  std::set<std::string> acc_dims;
+  std::vector<std::string> lines;
+
+  std::string ext_of(const std::string& d) const {
+    return d == e_index ? std::string("E") : std::to_string(ext.at(d));
+  }
+  std::string offset(const std::string& name, const std::vector<std::string>& idx) const {
+    const auto& dd = dims.at(name);
+    if (idx.size() != dd.size()) irfail(name + " subscripted with the wrong rank");
+    if (idx.empty()) return "0";
+    std::string e = "(long)i_" + idx[0];
+    for (size_t i = 1; i < dd.size(); ++i) e = "(" + e + " * " + ext_of(dd[i]) + " + i_" + idx[i] + ")";
+    return e;
+  }
+  std::string temp_flat(const std::string& name, const std::vector<std::string>& idx) const {
+    const auto& td = temps.at(name);
+    if (idx.size() != td.size()) irfail("temporary " + name + " subscript count");
+    std::string f = "0";
+    for (size_t i = 0; i < td.size(); ++i)
+      f = "(" + f + " * " + std::to_string(ext.at(td[i])) + " + i_" + idx[i] + ")";
+    return f;
+  }
+  std::string expr(const Json& x, int prec) const {
+    if (x.kind == Json::Num) {
+      std::string s = lit(x.num);
+      return (x.num < 0 && prec >= 1) ? "(" + s + ")" : s;
+    }
+    if (x.kind == Json::Str) {
+      if (temps.count(x.str)) {
+        if (!temps.at(x.str).empty()) irfail("array temporary " + x.str + " read without subscripts");
+        return "v_" + ident(x.str);
+      }
+      if (consts.count(x.str)) return "c_" + ident(x.str);
+      irfail("unknown scalar '" + x.str + "'");
+    }
+    if (x.kind != Json::Arr || x.arr.empty() || x.arr[0].kind != Json::Str) irfail("bad expression");
+    const std::string& op = x.arr[0].str;
+    if (op == "sym") {
+      const std::string& name = x.arr.at(1).str;
+      std::vector<std::string> idx;
+      for (size_t i = 2; i < x.arr.size(); ++i) idx.push_back(x.arr[i].str);
+      if (tabs.count(name)) return "t_" + ident(name) + "[" + offset(name, idx) + "]";
+      if (temps.count(name)) return "v_" + ident(name) + "[" + temp_flat(name, idx) + "]";
+      if (outs.count(name)) return "o_" + ident(name) + "[" + offset(name, idx) + "]";
+      irfail("unknown array '" + name + "'");
+    }
+    if (op == "+" || op == "*") {
+      std::string s;
+      for (size_t i = 1; i < x.arr.size(); ++i) {
+        if (i > 1) s += op == "+" ? " + " : " * ";
+        s += expr(x.arr[i], op == "+" ? 0 : 1);
+      }
+      const int wrap_at = op == "+" ? 1 : 2;
+      return prec >= wrap_at ? "(" + s + ")" : s;
+    }
+    if (op == "/") {
+      if (x.arr.size() != 3) irfail("'/' takes two operands");
+      std::string s = expr(x.arr[1], 1) + " / " + expr(x.arr[2], 2);
+      return prec >= 2 ? "(" + s + ")" : s;
+    }
+    if (op == "call") {
+      const std::string& fn = x.arr.at(1).str;
+      auto it = calls().find(fn);
+      if (it == calls().end()) irfail("unsupported call '" + fn + "'");
+      std::string s = it->second + "(";
+      for (size_t i = 2; i < x.arr.size(); ++i) {
+        if (i > 2) s += ", ";
+        s += expr(x.arr[i], 0);
+      }
+      return s + ")";
+    }
+    irfail("unknown operator '" + op + "'");
+  }
+  void emit_nodes(const std::vector<Node>& nodes, int ind) {
+    const std::string pad(2 * ind, ' ');
+    for (const Node& n : nodes) {
+      if (n.loop) {
+        if (n.index == e_index) irfail("nested element loop");
+        if (warp && n.index == J) {
+          lines.push_back(pad + "#pragma unroll");
+          lines.push_back(pad + "for (int r_ = 0; r_ < " + std::to_string(R) + "; ++r_) {");
+          lines.push_back(pad + "  const int i_" + ident(J) + " = lane_ + 32 * r_;");
+          lines.push_back(pad + "  if (i_" + J + " < " + std::to_string(n.end) + ") {");
+          emit_nodes(n.body, ind + 2);
+          lines.push_back(pad + "  }");
+          lines.push_back(pad + "}");
+          continue;
+        }
+        if (warp && n.end - n.begin <= 64 && acc_dims.count(n.index)) {
+          double t[2] = {0, 0};
+          op_counts(n.body, 1, false, "", t);
+          if ((n.end - n.begin) * t[0] <= 4096) lines.push_back(pad + "#pragma unroll");
+        }
+        lines.push_back(pad + "for (int i_" + ident(n.index) + " = " + std::to_string(n.begin) + "; i_" +
+                        n.index + " < " + std::to_string(n.end) + "; ++i_" + n.index + ") {");
+        emit_nodes(n.body, ind + 1);
+        lines.push_back(pad + "}");
+      } else {
+        std::string target;
+        if (outs.count(n.name) && warp) {
+          std::string f = "0";
+          const auto& dd = dims.at(n.name);
+          for (size_t i = 2; i < dd.size(); ++i)
+            f = "(" + f + " * " + std::to_string(ext.at(dd[i])) + " + i_" + n.idx[i] + ")";
+          target = "a_" + n.name + "[r_ * " + std::to_string(rest.at(n.name)) + " + " + f + "]";
+        } else if (outs.count(n.name)) {
+          target = "o_" + n.name + "[" + offset(n.name, n.idx) + "]";
+        } else if (!temps.at(n.name).empty()) {
+          target = "v_" + n.name + "[" + temp_flat(n.name, n.idx) + "]";
+        } else {
+          target = "v_" + n.name;
+        }
+        if (n.op == "+=")
+          lines.push_back(pad + target + " += " + expr(*n.rhs, 0) + ";");
+        else if (n.op == "=")
+          lines.push_back(pad + target + " = " + expr(*n.rhs, 0) + ";");
+        else
+          irfail("unknown assignment '" + n.op + "'");
+      }
+    }
+  }
+};
+
+struct Kernel {
+  std::string source, fn = "femopt_kernel", cls_strategy;
+  std::vector<std::string> outputs, inputs, constants, preevaluated;
+  std::map<std::string, std::vector<std::string>> dims;
+  std::map<std::string, long> ext;
+  std::string e_index;
+  bool warp = false;
+  std::vector<char> cubin;
+  cudaLibrary_t lib = nullptr;
+  cudaKernel_t kern = nullptr;
+  int device = -1;
+
+  long size_of(const std::string& name, long ncells) const {
+    long s = 1;
+    for (const auto& d : dims.at(name)) s *= d == e_index ? ncells : ext.at(d);
+    return s;
+  }
+};
+
+bool warp_plan(const std::vector<Node>& tree, Emitter& em) {
+  if (em.e_index.empty()) return false;
+  std::set<std::pair<std::string, std::string>> rows;
+  for (const auto& o : em.outs) {
+    const auto& d = em.dims.at(o);
+    if (d.size() < 2) return false;
+    rows.insert({d[0], d[1]});
+  }
+  if (rows.size() != 1 || rows.begin()->first != em.e_index) return false;
+  const std::string J = rows.begin()->second;
+  bool ok = true;
+  std::set<std::string> written_in_J, read_outside_J;
+  std::function<void(const std::vector<Node>&, bool)> walk = [&](const std::vector<Node>& ns,
+                                                                 bool inJ) {
+    for (const Node& n : ns) {
+      if (n.loop) {
+        if (n.index == J) {
+          if (inJ || n.begin != 0 || n.end != em.ext.at(J)) ok = false;
+          walk(n.body, true);
+        } else {
+          walk(n.body, inJ);
+        }
+      } else {
+        std::set<std::string> used;
+        names_in(*n.rhs, used);
+        for (const auto& o : em.outs)
+          if (used.count(o)) ok = false;
+        if (em.outs.count(n.name)) {
+          if (!inJ || n.op != "+=" || n.idx.size() < 2 || n.idx[0] != em.e_index || n.idx[1] != J)
+            ok = false;
+        } else if (inJ) {
+          written_in_J.insert(n.name);
+        }
+        if (!inJ) read_outside_J.insert(used.begin(), used.end());
+      }
+    }
+  };
+  walk(tree, false);
+  for (const auto& w : written_in_J)
+    if (read_outside_J.count(w)) ok = false;
+  if (ok) em.J = J;
+  return ok;
+}
+
+void scan(const std::vector<Node>& nodes, Emitter& em) {
+  for (const Node& n : nodes) {
+    if (n.loop) {
+      scan(n.body, em);
+      continue;
+    }
+    if (em.outs.count(n.name)) {
+      auto it = em.dims.find(n.name);
+      if (it != em.dims.end() && it->second != n.idx) irfail("output " + n.name + " written with different subscripts");
+      em.dims[n.name] = n.idx;
+    } else if (em.tabs.count(n.name)) {
+      irfail("statement writes table " + n.name);
+    } else {
+      auto it = em.temps.find(n.name);
+      if (it != em.temps.end() && it->second != n.idx) irfail("temporary " + n.name + " used with different subscripts");
+      em.temps[n.name] = n.idx;
+    }
+  }
+}
+
+std::unique_ptr<Kernel> generate(const char* json, int strategy) {
+  Json ir = parse(json);
+  auto K = std::make_unique<Kernel>();
+  Emitter em;
+  for (const auto& kv : ir.at("indices").obj) em.ext[kv.first] = (long)kv.second.num;
+  const Json* T = ir.get("tables");
+  std::map<std::string, const Json*> tables;
+  if (T)
+    for (const auto& kv : T->obj) {
+      tables[kv.first] = &kv.second;
+      em.tabs.insert(kv.first);
+      std::vector<std::string> dd;
+      for (const auto& d : kv.second.at("dims").arr) dd.push_back(d.str);
+      em.dims[kv.first] = dd;
+    }
+  const Json* C = ir.get("constants");
+  std::map<std::string, double> cvals;
+  if (C && C->kind == Json::Obj)
+    for (const auto& kv : C->obj) {
+      em.consts.insert(kv.first);
+      cvals[kv.first] = kv.second.num;
+    }
+  for (const auto& o : ir.at("outputs").arr) em.outs.insert(o.str);
+  std::vector<Node> tree = build_tree(ir, em.ext);
+
+  std::vector<const Node*> top;
+  for (const Node& n : tree)
+    if (n.loop) top.push_back(&n);
+  if (top.size() == 1 && (top[0]->cls == "orderfree" || (top[0]->cls.empty() && top[0]->index == "e")))
+    em.e_index = top[0]->index;
+  scan(tree, em);
+  for (const auto& o : em.outs)
+    if (!em.dims.count(o)) irfail("output " + o + " is never written");
+
+  const bool can_warp = warp_plan(tree, em);
+  bool warp = false;
+  if (strategy == 0) {
+    if (can_warp && em.ext.at(em.J) >= 8) {
+      double t[2] = {0, 0};
+      op_counts(tree, 1, false, em.J, t);
+      warp = 31 * t[0] < 0.25 * t[1];
+    }
+  } else if (strategy == 2) {
+    if (!can_warp) irfail("the warp mapping does not apply to this nest");
+    warp = true;
+  } else if (strategy != 1) {
+    irfail("unknown strategy");
+  }
+  em.warp = warp;
+  if (warp) {
+    em.R = (em.ext.at(em.J) + 31) / 32;
+    for (const auto& o : em.outs) {
+      long r = 1;
+      const auto& dd = em.dims.at(o);
+      for (size_t i = 2; i < dd.size(); ++i) r *= em.ext.at(dd[i]), em.acc_dims.insert(dd[i]);
+      em.rest[o] = r;
+    }
+  }
+
+  for (const auto& kv : tables) {
+    const Json* pv = kv.second->get("provenance");
+    const bool pre = pv && pv->kind == Json::Str && pv->str == "preevaluated";
+    (pre ? K->preevaluated : K->inputs).push_back(kv.first);
+  }
+  K->outputs.assign(em.outs.begin(), em.outs.end());
+  K->constants.assign(em.consts.begin(), em.consts.end());
+  std::sort(K->inputs.begin(), K->inputs.end());
+  std::sort(K->preevaluated.begin(), K->preevaluated.end());
+
+  // body
+  std::vector<Node> pre, body;
+  if (!em.e_index.empty()) {
+    for (const Node& n : tree)
+      if (&n != top[0]) pre.push_back(n);
+    body = top[0]->body;
+  } else {
+    body = tree;
+  }
+  for (const Node& n : pre)
+    if (!n.loop && em.outs.count(n.name)) irfail("output written outside the element loop");
+  em.emit_nodes(pre, 1);
+  if (warp) {
+    em.lines.push_back("  const long i_" + em.e_index + " = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;");
+    em.lines.push_back("  const int lane_ = threadIdx.x & 31;");
+    em.lines.push_back("  if (i_" + em.e_index + " >= E) return;");
+    for (const auto& o : em.outs) {
+      const std::string n = std::to_string(em.R * em.rest[o]);
+      em.lines.push_back("  double a_" + o + "[" + n + "];");
+      em.lines.push_back("  #pragma unroll");
+      em.lines.push_back("  for (int x_ = 0; x_ < " + n + "; ++x_) a_" + o + "[x_] = 0.0;");
+    }
+  } else if (!em.e_index.empty()) {
+    em.lines.push_back("  const long i_" + em.e_index + " = (long)blockIdx.x * blockDim.x + threadIdx.x;");
+    em.lines.push_back("  if (i_" + em.e_index + " >= E) return;");
+  } else {
+    em.lines.push_back("  if (blockIdx.x != 0 || threadIdx.x != 0) return;");
+  }
+  em.emit_nodes(body, 1);
+  if (warp) {
+    const std::string nJ = std::to_string(em.ext.at(em.J)), R = std::to_string(em.R);
+    for (const auto& o : em.outs) {
+      const std::string rs = std::to_string(em.rest[o]);
+      em.lines.push_back("  #pragma unroll");
+      em.lines.push_back("  for (int r_ = 0; r_ < " + R + "; ++r_) {");
+      em.lines.push_back("    const long row_ = lane_ + 32 * r_;");
+      em.lines.push_back("    if (row_ < " + nJ + ") {");
+      em.lines.push_back("      double* dst_ = o_" + o + " + (i_" + em.e_index + " * " + nJ + " + row_) * " + rs + ";");
+      em.lines.push_back("      for (int x_ = 0; x_ < " + rs + "; ++x_) dst_[x_] += a_" + o + "[r_ * " + rs + " + x_];");
+      em.lines.push_back("    }");
+      em.lines.push_back("  }");
+    }
+  }
+
+  std::string src = "// generated by libfemgpu (femgpu_ir_create) from a femopt kernel IR\n";
+  for (const auto& name : K->preevaluated) {
+    const Json& vals = tables[name]->at("values");
+    src += "__device__ const double t_" + ident(name) + "[" + std::to_string(std::max<size_t>(1, vals.arr.size())) + "] = {";
+    for (size_t i = 0; i < vals.arr.size(); ++i) {
+      if (i) src += ",";
+      src += lit(vals.arr[i].num);
+    }
+    src += "};\n";
+  }
+  src += "extern \"C\" __global__ void __launch_bounds__(128) " + K->fn + "(";
+  std::vector<std::string> params;
+  for (const auto& o : K->outputs) params.push_back("double* __restrict__ o_" + ident(o));
+  for (const auto& t : K->inputs) params.push_back("const double* __restrict__ t_" + ident(t));
+  for (const auto& c : K->constants) params.push_back("const double c_" + ident(c));
+  params.push_back("const long E");
+  for (size_t i = 0; i < params.size(); ++i) src += (i ? ", " : "") + params[i];
+  src += ") {\n";
+  for (const auto& kv : em.temps) {
+    if (!kv.second.empty()) {
+      long n = 1;
+      for (const auto& d : kv.second) {
+        if (d == em.e_index) irfail("temporary " + kv.first + " indexed by the element loop");
+        n *= em.ext.at(d);
+      }
+      src += "  double v_" + ident(kv.first) + "[" + std::to_string(n) + "];\n";
+    } else {
+      src += "  double v_" + ident(kv.first) + ";\n";
+    }
+  }
+  for (const auto& l : em.lines) src += l + "\n";
+  src += "}\n";
+  K->source = src;
+  K->dims = em.dims;
+  K->ext = em.ext;
+  K->e_index = em.e_index;
+  K->warp = warp;
+  return K;
+}
+
+// ----------------------------------------------------------------------------
+// NVRTC (dlopen) and module load
+// ----------------------------------------------------------------------------
+struct Nvrtc {
+  void* h = nullptr;
+  int (*create)(void**, const char*, const char*, int, const char* const*, const char* const*) = nullptr;
+  int (*compile)(void*, int, const char* const*) = nullptr;
+  int (*logsize)(void*, size_t*) = nullptr;
+  int (*log)(void*, char*) = nullptr;
+  int (*cubinsize)(void*, size_t*) = nullptr;
+  int (*cubin)(void*, char*) = nullptr;
+  int (*destroy)(void**) = nullptr;
+};
+
+const Nvrtc& nvrtc() {
+  static Nvrtc n;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    for (const char* name : {"libnvrtc.so.12", "libnvrtc.so", "/usr/local/cuda/lib64/libnvrtc.so.12"}) {
+      n.h = dlopen(name, RTLD_NOW | RTLD_LOCAL);
+      if (n.h) break;
+    }
+    if (!n.h) return;
+    n.create = (decltype(n.create))dlsym(n.h, "nvrtcCreateProgram");
+    n.compile = (decltype(n.compile))dlsym(n.h, "nvrtcCompileProgram");
+    n.logsize = (decltype(n.logsize))dlsym(n.h, "nvrtcGetProgramLogSize");
+    n.log = (decltype(n.log))dlsym(n.h, "nvrtcGetProgramLog");
+    n.cubinsize = (decltype(n.cubinsize))dlsym(n.h, "nvrtcGetCUBINSize");
+    n.cubin = (decltype(n.cubin))dlsym(n.h, "nvrtcGetCUBIN");
+    n.destroy = (decltype(n.destroy))dlsym(n.h, "nvrtcDestroyProgram");
+  });
+  if (!n.h || !n.create || !n.compile || !n.cubin)
+    throw CudaError("CUDA: NVRTC (libnvrtc.so.12) is not available");
+  return n;
+}
+
+void compile(Kernel& K) {
+  const Nvrtc& nv = nvrtc();
+  void* prog = nullptr;
+  if (nv.create(&prog, K.source.c_str(), "femopt_kernel.cu", 0, nullptr, nullptr) != 0)
+    throw CudaError("CUDA: nvrtcCreateProgram failed");
+  const char* opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "--prec-div=true",
+                        "--prec-sqrt=true", "-std=c++17", "-default-device"};
+  const int rc = nv.compile(prog, 6, opts);
+  if (rc != 0) {
+    size_t n = 0;
+    nv.logsize(prog, &n);
+    std::string log(n, '\0');
+    nv.log(prog, log.data());
+    nv.destroy(&prog);
+    throw CudaError("CUDA: NVRTC compile failed:\n" + log);
+  }
+  size_t n = 0;
+  nv.cubinsize(prog, &n);
+  K.cubin.resize(n);
+  nv.cubin(prog, K.cubin.data());
+  nv.destroy(&prog);
+}
+
+}  // namespace irgen
+
+// ============================================================================
+// C ABI
+// ============================================================================
+struct femgpu_ir {
+  std::unique_ptr<irgen::Kernel> k;
+  std::mutex mu;
+};
+
+namespace {
+template <class Fn>
+int ir_guard(Fn&& fn) {
+  try {
+    fn();
+    femgpu::set_last_error("");
+    return FEMGPU_OK;
+  } catch (const irgen::IRError& e) {
+    femgpu::set_last_error(e.what());
+    return FEMGPU_ERR_NOT_FEM_NEST;
+  } catch (const irgen::CudaError& e) {
+    femgpu::set_last_error(e.what());
+    return FEMGPU_ERR_CUDA;
+  } catch (const std::exception& e) {
+    femgpu::set_last_error(e.what());
+    return FEMGPU_ERR_INTERNAL;
+  }
+}
+
+int bad_arg(const char* m) {
+  femgpu::set_last_error(m);
+  return FEMGPU_ERR_INVALID_ARG;
+}
+
+void cuda_ok(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw irgen::CudaError(std::string("CUDA ") + what + ": " + cudaGetErrorString(e));
+}
+
+cudaKernel_t loaded(femgpu_ir* f) {
+  std::lock_guard<std::mutex> lock(f->mu);
+  auto& K = *f->k;
+  int dev = 0;
+  cuda_ok(cudaGetDevice(&dev), "cudaGetDevice");
+  if (!K.kern || K.device != dev) {
+    cuda_ok(cudaLibraryLoadData(&K.lib, K.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0),
+            "cudaLibraryLoadData");
+    cuda_ok(cudaLibraryGetKernel(&K.kern, K.lib, K.fn.c_str()), "cudaLibraryGetKernel");
+    K.device = dev;
+  }
+  return K.kern;
+}
+}  // namespace
+
+extern "C" {
+
+int femgpu_ir_create(const char* json, int strategy, femgpu_ir** out) {
+  if (!json || !out) return bad_arg("null argument");
+  *out = nullptr;
+  return ir_guard([&] {
+    auto f = std::make_unique<femgpu_ir>();
+    f->k = irgen::generate(json, strategy);
+    irgen::compile(*f->k);
+    *out = f.release();
+  });
+}
+
+void femgpu_ir_free(femgpu_ir* f) {
+  if (f && f->k && f->k->lib) cudaLibraryUnload(f->k->lib);
+  delete f;
+}
+
+int femgpu_ir_get_info(const femgpu_ir* f, femgpu_ir_info* info) {
+  if (!f || !info) return bad_arg("null argument");
+  const auto& K = *f->k;
+  info->noutputs = (int)K.outputs.size();
+  info->ninputs = (int)K.inputs.size();
+  info->nconstants = (int)K.constants.size();
+  info->per_cell = K.e_index.empty() ? 0 : 1;
+  info->strategy = K.warp ? 2 : 1;
+  return FEMGPU_OK;
+}
+
+int femgpu_ir_argname(const femgpu_ir* f, int group, int index, char* buf, size_t len) {
+  if (!f || !buf || group < 0 || group > 2) return bad_arg("bad argument");
+  const auto& v = group == 0 ? f->k->outputs : group == 1 ? f->k->inputs : f->k->constants;
+  if (index < 0 || index >= (int)v.size()) return bad_arg("argument index out of range");
+  std::snprintf(buf, len, "%s", v[index].c_str());
+  return FEMGPU_OK;
+}
+
+int femgpu_ir_arg_size(const femgpu_ir* f, int group, int index, long ncells, long* size) {
+  if (!f || !size || group < 0 || group > 1) return bad_arg("bad argument");
+  const auto& v = group == 0 ? f->k->outputs : f->k->inputs;
+  if (index < 0 || index >= (int)v.size()) return bad_arg("argument index out of range");
+  *size = f->k->size_of(v[index], ncells);
+  return FEMGPU_OK;
+}
+
+const char* femgpu_ir_source(const femgpu_ir* f) { return f ? f->k->source.c_str() : ""; }
+
+int femgpu_ir_launch(femgpu_ir* f, long ncells, double* const* outputs, const double* const* inputs,
+                     const double* constants, void* stream) {
+  if (!f || ncells < 0 || (!f->k->outputs.empty() && !outputs) ||
+      (!f->k->inputs.empty() && !inputs) || (!f->k->constants.empty() && !constants))
+    return bad_arg("bad argument");
+  return ir_guard([&] {
+    const auto& K = *f->k;
+    if (!K.e_index.empty() && ncells == 0) return;
+    cudaKernel_t kern = loaded(f);
+    std::vector<void*> args;
+    std::vector<const void*> ptrs(K.outputs.size() + K.inputs.size());
+    for (size_t i = 0; i < K.outputs.size(); ++i) ptrs[i] = outputs[i];
+    for (size_t i = 0; i < K.inputs.size(); ++i) ptrs[K.outputs.size() + i] = inputs[i];
+    for (auto& p : ptrs) args.push_back(&p);
+    std::vector<double> cv(K.constants.size());
+    for (size_t i = 0; i < cv.size(); ++i) {
+      cv[i] = constants[i];
+      args.push_back(&cv[i]);
+    }
+    long E = ncells;
+    args.push_back(&E);
+    const long threads = K.e_index.empty() ? 1 : ncells * (K.warp ? 32 : 1);
+    const unsigned grid = (unsigned)std::max<long>(1, (threads + 127) / 128);
+    cuda_ok(cudaLaunchKernel((const void*)kern, dim3(grid), dim3(128), args.data(), 0,
+                             static_cast<cudaStream_t>(stream)),
+            "cudaLaunchKernel");
+  });
+}
+
+int femgpu_ir_argv(femgpu_ir* f, long ncells, double* const* o, const double* const* t,
+                   const double* c) {
+  if (!f || ncells < 0) return bad_arg("bad argument");
+  return ir_guard([&] {
+    const auto& K = *f->k;
+    std::vector<double*> d_o(K.outputs.size()), d_t(K.inputs.size());
+    std::vector<long> so(K.outputs.size());
+    auto cleanup = [&] {
+      for (auto p : d_o) cudaFree(p);
+      for (auto p : d_t) cudaFree(p);
+    };
+    try {
+      for (size_t i = 0; i < K.outputs.size(); ++i) {
+        so[i] = K.size_of(K.outputs[i], ncells);
+        cuda_ok(cudaMalloc(&d_o[i], std::max<long>(1, so[i]) * sizeof(double)), "cudaMalloc");
+        cuda_ok(cudaMemcpy(d_o[i], o[i], so[i] * sizeof(double), cudaMemcpyHostToDevice), "H2D");
+      }
+      for (size_t i = 0; i < K.inputs.size(); ++i) {
+        const long s = K.size_of(K.inputs[i], ncells);
+        cuda_ok(cudaMalloc(&d_t[i], std::max<long>(1, s) * sizeof(double)), "cudaMalloc");
+        cuda_ok(cudaMemcpy(d_t[i], t[i], s * sizeof(double), cudaMemcpyHostToDevice), "H2D");
+      }
+      std::vector<const double*> ct(d_t.begin(), d_t.end());
+      const int rc = femgpu_ir_launch(f, ncells, d_o.data(), ct.data(), c, nullptr);
+      if (rc != FEMGPU_OK) throw irgen::CudaError(femgpu_last_error());
+      cuda_ok(cudaDeviceSynchronize(), "kernel");
+      for (size_t i = 0; i < K.outputs.size(); ++i)
+        cuda_ok(cudaMemcpy(o[i], d_o[i], so[i] * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
+  });
+}
+
+}  // extern "C"

@@ -41,7 +41,9 @@ ERROR_NAMES = {
 EXPORTS = ("femgpu_form_create", "femgpu_form_free", "femgpu_form_get_info", "femgpu_assemble",
            "femgpu_assemble_host", "femgpu_kernel_argv", "femgpu_kernel_argc",
            "femgpu_kernel_argname", "femgpu_gather", "femgpu_csr_positions",
-           "femgpu_scatter_add", "femgpu_last_error", "femgpu_version")
+           "femgpu_scatter_add", "femgpu_ir_create", "femgpu_ir_free", "femgpu_ir_get_info",
+           "femgpu_ir_argname", "femgpu_ir_arg_size", "femgpu_ir_source", "femgpu_ir_launch",
+           "femgpu_ir_argv", "femgpu_last_error", "femgpu_version")
 
 
 class FemgpuError(RuntimeError):

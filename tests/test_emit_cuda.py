@@ -33,19 +33,21 @@ def test_fixtures_present():
 
 
 @pytest.mark.parametrize("case", CASES)
-def test_emit_and_nvrtc_compile(case):
-    # no GPU needed: NVRTC cross-compiles the generated source for sm_100a
+def test_generate_and_nvrtc_compile(case):
+    # femgpu_ir_create parses, generates and NVRTC-compiles for sm_100a: no GPU needed
     js, d, _ = load(case)
-    em = emit_cuda.emit(js)
+    K = emit_cuda.IRKernel(js)
     tabs = d["tables"]
-    assert em.outputs == sorted(d["outputs"])
-    assert em.inputs == sorted(n for n, t in tabs.items()
-                               if t.get("provenance", "input") != "preevaluated")
-    assert em.preevaluated == sorted(n for n, t in tabs.items()
-                                     if t.get("provenance") == "preevaluated")
-    assert em.e_index == "e"
-    cubin = emit_cuda.compile_cubin(em.source)
-    assert cubin[:4] == b"\x7fELF"
+    assert K.outputs == sorted(d["outputs"])
+    assert K.inputs == sorted(n for n, t in tabs.items()
+                              if t.get("provenance", "input") != "preevaluated")
+    assert K.constants == sorted((d.get("constants") or {}).keys())
+    assert K.per_cell
+    src = K.source
+    for n in tabs:
+        if tabs[n].get("provenance") == "preevaluated":
+            assert f"__device__ const double t_{n}[" in src
+    assert "fma(" not in src  # the emitted arithmetic only
 
 
 def test_bad_ir_is_rejected():
@@ -55,11 +57,13 @@ def test_bad_ir_is_rejected():
     bad = json.loads(ir.dumps(k))
     bad["statements"][-1]["rhs"] = ["*", "nosuchscalar", 1.0]
     with pytest.raises(emit_cuda.IRError):
-        emit_cuda.emit(bad)
+        emit_cuda.IRKernel(bad)
     bad = json.loads(ir.dumps(k))
     bad["statements"][-1]["rhs"] = ["call", "system", 1.0]
     with pytest.raises(emit_cuda.IRError):
-        emit_cuda.emit(bad)
+        emit_cuda.IRKernel(bad)
+    with pytest.raises(emit_cuda.IRError):
+        emit_cuda.IRKernel('{"indices": {"e": 2}, "loops": [')
 
 
 # ----------------------------------------------------------------------------
@@ -69,7 +73,7 @@ def _strategies(case):
     js, _, _ = load(case)
     out = ["thread"]
     try:
-        emit_cuda.emit(js, strategy="warp")
+        emit_cuda.IRKernel(js, strategy="warp")
         out.append("warp")
     except emit_cuda.IRError:
         pass

@@ -52,13 +52,13 @@ def main(names):
         for oname, k in kernels:
             K = emit_cuda.IRKernel(k)
             inputs = {}
-            for n in K.em.inputs:
+            for n in K.inputs:
                 if n in et:
                     inputs[n] = et[n]
                 else:
                     inputs[n] = torch.tensor(np.asarray(k["tables"][n]["values"]), device=dev)
-            outs = {o: torch.zeros(K.em.size(o, E), dtype=torch.float64, device=dev)
-                    for o in K.em.outputs}
+            outs = {o: torch.zeros(K.size(0, o, E), dtype=torch.float64, device=dev)
+                    for o in K.outputs}
             K.run(outs, inputs, k.get("constants", {}), E)
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
