@@ -203,6 +203,14 @@ int femgpu_ir_launch(femgpu_ir* k, long ncells, double* const* outputs,
 int femgpu_ir_argv(femgpu_ir* k, long ncells, double* const* o, const double* const* t,
                    const double* c);
 
+/* The element matrices straight into the global CSR matrix:
+ * vals[pos[e][j][k]] += A_e[j][k] (pos from femgpu_csr_positions).  Fused into
+ * the element kernel's epilogue where that is faster (P1 Helmholtz: A_e never
+ * goes to HBM), else the element kernel into an L2-sized form-owned scratch
+ * followed by femgpu_scatter_add.  Device pointers; pos 16-byte aligned. */
+int femgpu_assemble_csr(const femgpu_form* f, long ncells, const double* coords,
+                        const double* coeffs, const long* pos, double* vals, void* stream);
+
 /* Message for the most recent failure on this thread ("" if none). */
 const char* femgpu_last_error(void);
 

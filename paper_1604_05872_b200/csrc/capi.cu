@@ -84,12 +84,17 @@ struct femgpu_form {
   cudaStream_t host_st[NSTREAM] = {nullptr, nullptr, nullptr};
   double* host_buf[NSTREAM] = {nullptr, nullptr, nullptr};
   long host_chunk = 0;
+  // scratch element matrices for femgpu_assemble_csr on routes without a fused epilogue
+  std::mutex csr_mu;
+  double* csr_scratch = nullptr;
+  long csr_chunk = 0;
 
   ~femgpu_form() {
     int cur = 0;
     cudaGetDevice(&cur);
     cudaSetDevice(device);
     if (d_tab) cudaFree(d_tab);
+    if (csr_scratch) cudaFree(csr_scratch);
     for (int i = 0; i < NSTREAM; ++i) {
       if (host_buf[i]) cudaFree(host_buf[i]);
       if (host_st[i]) cudaStreamDestroy(host_st[i]);
@@ -614,6 +619,53 @@ int femgpu_csr_positions(long ncells, int n, const int* dof_map, const long* row
     if (missing)
       throw Error(FEMGPU_ERR_INCONSISTENT_LAYOUT,
                   std::to_string(missing) + " element-matrix entries outside the CSR pattern");
+  });
+}
+
+int femgpu_assemble_csr(const femgpu_form* fc, long ncells, const double* coords,
+                        const double* coeffs, const long* pos, double* vals, void* stream) {
+  if (!fc) {
+    g_last_error = "null form";
+    return FEMGPU_ERR_INVALID_ARG;
+  }
+  femgpu_form* f = const_cast<femgpu_form*>(fc);  // scratch cache only; guarded below
+  return guarded([&] {
+    if (ncells < 0) throw Error(FEMGPU_ERR_INVALID_ARG, "negative cell count");
+    if (ncells == 0) return;
+    if (!coords || !pos || !vals || (f->ncoef > 0 && !coeffs))
+      throw Error(FEMGPU_ERR_INVALID_ARG, "null buffer");
+    check_ptr(coords, "coords");
+    if (f->ncoef > 0) check_ptr(coeffs, "coeffs");
+    check_ptr(pos, "pos");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int cur = 0;
+    cuda_check(cudaGetDevice(&cur), "cudaGetDevice");
+    if (cur != f->device) throw Error(FEMGPU_ERR_INVALID_ARG, "form belongs to another device");
+    if (f->route == ROUTE_HELM_P1) {  // fused epilogue: A_e never leaves the SM
+      cuda_check(femgpu::launch_helm_p1(f->p1, ncells, coords, coeffs, nullptr, 0, s, pos, vals),
+                 f->kernel_name.c_str());
+      return;
+    }
+    // element kernel into a form-owned scratch, then the scatter-add (chunks of
+    // ~256 MiB, L2-friendly).  A fused copy-out in the warp-specialised tensor
+    // kernels was measured slower: its 4 IO warps cannot issue the atomics of a
+    // 32-cell tile in the time the MMA warps take (c2: 4.5 vs 3.0 ms).
+    std::lock_guard<std::mutex> lock(f->csr_mu);
+    const size_t nn = (size_t)f->n * f->n;
+    const long chunk = std::max<long>(64, (long)((256u << 20) / (nn * 8)) / 64 * 64);
+    if (!f->csr_scratch || f->csr_chunk != chunk) {
+      if (f->csr_scratch) cudaFree(f->csr_scratch);
+      f->csr_scratch = nullptr;
+      cuda_check(cudaMalloc(&f->csr_scratch, chunk * nn * sizeof(double)), "cudaMalloc(scratch)");
+      f->csr_chunk = chunk;
+    }
+    for (long c0 = 0; c0 < ncells; c0 += chunk) {
+      const long E = std::min(chunk, ncells - c0);
+      launch(f, E, coords + c0 * 12, f->ncoef > 0 ? coeffs + c0 * f->ncoef : coeffs,
+             f->csr_scratch, 0, s);
+      cuda_check(femgpu::launch_scatter_add(E * (long)nn, f->csr_scratch, pos + c0 * (long)nn, vals, s),
+                 "scatter_add_kernel");
+    }
   });
 }
 

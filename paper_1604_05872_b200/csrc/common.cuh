@@ -134,6 +134,15 @@ __device__ __forceinline__ double2 ldg_stream(const double2* p) {
   return v;
 }
 
+// read-once 16-byte load of index data (no L1 allocation)
+__device__ __forceinline__ longlong2 ldg_stream_idx(const longlong2* p) {
+  longlong2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.s64 {%0,%1}, [%2];\n"
+               : "=l"(v.x), "=l"(v.y)
+               : "l"(p));
+  return v;
+}
+
 __device__ __forceinline__ void stg_stream(double2* p, double2 v) {
   asm volatile("st.global.cs.v2.f64 [%0], {%1,%2};\n" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
 }

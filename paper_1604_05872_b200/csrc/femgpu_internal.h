@@ -18,8 +18,10 @@ struct HelmP1Params {
   double Dr[4][3];  // constant reference gradients, Dr[j][a] = D[a][*][j]
 };
 
+// pos/vals non-null: fused global assembly (vals[pos] += A_e) instead of writing A
 cudaError_t launch_helm_p1(const HelmP1Params& prm, long E, const double* coords,
-                           const double* coef, double* A, int acc, cudaStream_t s);
+                           const double* coef, double* A, int acc, cudaStream_t s,
+                           const long* pos = nullptr, double* vals = nullptr);
 
 bool helm_tensor_supported(int ns, int nc);
 void helm_tensor_geometry(int ns, int nc, int* KS, int* NT, int* KR, int* NP);

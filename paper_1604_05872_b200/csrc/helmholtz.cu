@@ -43,7 +43,8 @@ constexpr size_t P1_SMEM = sizeof(double) * (P1_NBUF * P1_IN + P1_TILE * P1_SO) 
 template <bool ACC>
 __global__ void __launch_bounds__(P1_TILE, P1_CTAS)
     helm_p1_kernel(HelmP1Params prm, long E, const double* __restrict__ coords,
-                   const double* __restrict__ coef, double* __restrict__ A) {
+                   const double* __restrict__ coef, double* __restrict__ A,
+                   const long* __restrict__ pos, double* __restrict__ vals) {
   extern __shared__ __align__(16) double smem[];
   double* sIn = smem;                               // [NBUF][coords 128x12 | f 128x4]
   double* so = smem + P1_NBUF * P1_IN;              // [128][18]
@@ -127,6 +128,19 @@ __global__ void __launch_bounds__(P1_TILE, P1_CTAS)
       if (i < nt * 8) v[u] = *reinterpret_cast<const double2*>(&so[(i / 8) * P1_SO + 2 * (i % 8)]);
     }
     __syncthreads();  // staging free for the next tile
+    if (pos) {  // fused global assembly: vals[pos] += A_e (CSR positions, global.cu)
+      const long* gp = pos + e0 * 16;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = u * P1_TILE + tid;
+        if (i < nt * 8) {
+          const longlong2 p = ldg_stream_idx(reinterpret_cast<const longlong2*>(gp) + i);
+          atomicAdd(vals + p.x, v[u].x);
+          atomicAdd(vals + p.y, v[u].y);
+        }
+      }
+      continue;
+    }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int i = u * P1_TILE + tid;
@@ -143,7 +157,8 @@ __global__ void __launch_bounds__(P1_TILE, P1_CTAS)
 }
 
 cudaError_t launch_helm_p1(const HelmP1Params& prm, long E, const double* coords,
-                           const double* coef, double* A, int acc, cudaStream_t s) {
+                           const double* coef, double* A, int acc, cudaStream_t s,
+                           const long* pos, double* vals) {
   if (E <= 0) return cudaSuccess;
   static bool configured = false;
   if (!configured) {
@@ -158,9 +173,9 @@ cudaError_t launch_helm_p1(const HelmP1Params& prm, long E, const double* coords
   const long maxc = (long)P1_CTAS * kNumSMs;
   const int grid = (int)(ntiles < maxc ? ntiles : maxc);
   if (acc)
-    helm_p1_kernel<true><<<grid, P1_TILE, P1_SMEM, s>>>(prm, E, coords, coef, A);
+    helm_p1_kernel<true><<<grid, P1_TILE, P1_SMEM, s>>>(prm, E, coords, coef, A, pos, vals);
   else
-    helm_p1_kernel<false><<<grid, P1_TILE, P1_SMEM, s>>>(prm, E, coords, coef, A);
+    helm_p1_kernel<false><<<grid, P1_TILE, P1_SMEM, s>>>(prm, E, coords, coef, A, pos, vals);
   return cudaGetLastError();
 }
 

@@ -41,7 +41,7 @@ ERROR_NAMES = {
 EXPORTS = ("femgpu_form_create", "femgpu_form_free", "femgpu_form_get_info", "femgpu_assemble",
            "femgpu_assemble_host", "femgpu_kernel_argv", "femgpu_kernel_argc",
            "femgpu_kernel_argname", "femgpu_gather", "femgpu_csr_positions",
-           "femgpu_scatter_add", "femgpu_ir_create", "femgpu_ir_free", "femgpu_ir_get_info",
+           "femgpu_scatter_add", "femgpu_assemble_csr", "femgpu_ir_create", "femgpu_ir_free", "femgpu_ir_get_info",
            "femgpu_ir_argname", "femgpu_ir_arg_size", "femgpu_ir_source", "femgpu_ir_launch",
            "femgpu_ir_argv", "femgpu_last_error", "femgpu_version")
 
@@ -94,6 +94,7 @@ def lib():
         L.femgpu_gather.argtypes = [C.c_long, C.c_int, vp, vp, vp, vp, vp, vp, vp]
         L.femgpu_csr_positions.argtypes = [C.c_long, C.c_int, vp, vp, vp, vp, vp]
         L.femgpu_scatter_add.argtypes = [C.c_long, vp, vp, vp, vp]
+        L.femgpu_assemble_csr.argtypes = [vp, C.c_long, vp, vp, vp, vp, vp]
         _lib = L
     return _lib
 
@@ -166,6 +167,15 @@ class Form:
         s = None if stream is None else (stream if isinstance(stream, int) else stream.cuda_stream)
         _check(lib().femgpu_assemble(self.h, E, _devptr(coords), _devptr(coeffs), _devptr(out),
                                      int(accumulate), s))
+
+    def assemble_csr(self, coords, coeffs, pos, vals, ncells: int | None = None, stream=None):
+        """Element matrices straight into CSR values: vals[pos] += A_e (device tensors;
+        pos from csr_positions).  Fused into the element kernel where it has a
+        CSR epilogue (Helmholtz), else kernel + scatter-add."""
+        E = int(coords.shape[0]) if ncells is None else int(ncells)
+        s = None if stream is None else (stream if isinstance(stream, int) else stream.cuda_stream)
+        _check(lib().femgpu_assemble_csr(self.h, E, _devptr(coords), _devptr(coeffs),
+                                         _devptr(pos), _devptr(vals), s))
 
     # -- host path (end to end) ----------------------------------------------
     def assemble_host(self, coords: np.ndarray, coeffs: np.ndarray, out: np.ndarray | None = None,

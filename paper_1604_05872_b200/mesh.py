@@ -171,12 +171,17 @@ class GlobalAssembler:
 
         femgpu.gather(self.V, self.cells, coef, self.coef_idx, self.coords, self.coeffs, stream)
 
-    def assemble(self, coef, stream=None):
-        """CSR values of the global matrix for global coefficient vector ``coef``."""
+    def assemble(self, coef, stream=None, fused: bool = True):
+        """CSR values of the global matrix for global coefficient vector ``coef``.
+        ``fused``: element kernel and scatter in one launch (femgpu_assemble_csr);
+        otherwise A_e is materialised in ``self.A`` and scatter-added."""
         from . import femgpu
 
         self.gather(coef, stream)
-        self.form.assemble(self.coords, self.coeffs, self.A, stream=stream)
         self.vals.zero_()
-        femgpu.scatter_add(self.A, self.pos, self.vals, stream)
+        if fused:
+            self.form.assemble_csr(self.coords, self.coeffs, self.pos, self.vals, stream=stream)
+        else:
+            self.form.assemble(self.coords, self.coeffs, self.A, stream=stream)
+            femgpu.scatter_add(self.A, self.pos, self.vals, stream)
         return self.vals

@@ -66,7 +66,8 @@ def test_gather_assemble_scatter(name):
     g = ga.mesh
     coef_np = g.global_coeffs()
     coef = torch.from_numpy(coef_np).to(ga.dev)
-    vals = ga.assemble(coef)
+    vals = ga.assemble(coef, fused=False).clone()
+    fused = ga.assemble(coef, fused=True).clone()
     torch.cuda.synchronize()
     # gather: exact copies
     _, cidx, _ = g.coef_layout()
@@ -78,6 +79,8 @@ def test_gather_assemble_scatter(name):
     ref = g.assemble_csr_host(ga.A.cpu().numpy(), row_ptr, col_idx)
     got = vals.cpu().numpy()
     assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max()
+    # femgpu_assemble_csr (fused epilogue for Helmholtz, kernel + scatter otherwise)
+    assert np.abs(fused.cpu().numpy() - ref).max() <= 1e-13 * np.abs(ref).max()
     # the element matrices are the path's own (pinned by the parity suite)
     if cfg.kind != fe.BURGERS:
         M = ga.form.assemble_host(ga.coords.cpu().numpy(), ga.coeffs.cpu().numpy())
