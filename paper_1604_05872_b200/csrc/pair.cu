@@ -44,13 +44,21 @@
 #ifndef PAIR_QUNROLL
 #define PAIR_QUNROLL 4  // q-loop unroll of the accumulate phase (measured: 1.56 -> 1.48 ms on c4)
 #endif
+#ifndef PAIR_WS_QUNROLL
+#define PAIR_WS_QUNROLL 8  // elasticity consumers (Q = 8; measured 1.081 -> 1.011 ms on c3 vs 1)
+#endif
 #ifndef PAIR_ELAS_FLAT
 #define PAIR_ELAS_FLAT 0
+#endif
+#ifndef PAIR_ABL  // development ablations of pair_ws_kernel: bit 0 no accumulate, bit 1 no store,
+                  // bit 2 no records, bit 3 no geometry, bit 4 no staging
+#define PAIR_ABL 0
 #endif
 
 namespace femgpu {
 
 constexpr int kPairQUnroll = PAIR_QUNROLL;
+constexpr int kPairWsQUnroll = PAIR_WS_QUNROLL;
 
 template <int KIND, int NS, int Q>
 struct PairShape {
@@ -69,16 +77,24 @@ struct PairShape {
   static constexpr int NCHUNK = (Q + QC - 1) / QC;
   static constexpr int RECD = SVK ? 9 : 3;               // per (q,j): g | h | s
   static constexpr int QSD = SVK ? 8 : 2;                // per q: lam', mu' | F F^T (6)
-  // j-stride of a record buffer: RECD*CELLS + 4 doubles, so the k-side loads of the
-  // (j,k) tiles sharing a warp (k0 two apart) fall in alternate bank halves
-  static constexpr int JS = RECD * CELLS + 4;
+  // ws (elasticity): each warp owns WCELLS cells of the tile (see pair_slot)
+  static constexpr bool WARP_CELLS = !FLAT;
+  static constexpr int WCELLS = CELLS / (ACC / 32);
+  // j-stride of a record buffer.  flat: RECD*CELLS + 4 doubles, so the k-side loads
+  // of the (j,k) tiles sharing a warp (k0 two apart) fall in alternate bank halves;
+  // ws: == 1 mod 8, so the 5 even k0 rows x WCELLS cells of a warp's load hit
+  // distinct banks (one wavefront)
+  static constexpr int JS = WARP_CELLS ? RECD * CELLS + 1 : RECD * CELLS + 4;
   static constexpr int REC_DBL = QC * (NS * JS + QSD * CELLS);  // one record buffer
   static constexpr int CSTRIDE = N * N + 2;              // staging stride: (stride/2) odd
   static constexpr int STG_DBL = CELLS * CSTRIDE;
   static constexpr int TAB0 = Q + 3 * Q * NS + 4 * Q;    // W | D | P
   static constexpr int TAB = (TAB0 + 1) / 2 * 2;
   static constexpr int CELLD = 10;                       // K(9), adet
-  static constexpr int IN_DBL = CELLS * (12 + NCOEF);    // raw inputs
+  // ws: coefficient rows padded to an odd stride (the producer's per-(cell, q) reads
+  // of 8 cells' rows are conflict-free)
+  static constexpr int CF = WARP_CELLS ? NCOEF + 1 : NCOEF;
+  static constexpr int IN_DBL = CELLS * (12 + CF);       // raw inputs
   static constexpr int HEAD = TAB + CELLS * CELLD + (FLAT ? 1 : 2) * IN_DBL;  // ws: double-buffered inputs
   // ws: two record buffers + separate staging; flat: one record buffer aliasing staging
   static constexpr int BODY = FLAT ? (REC_DBL > STG_DBL ? REC_DBL : STG_DBL)
@@ -86,6 +102,8 @@ struct PairShape {
   static constexpr size_t SMEM = sizeof(double) * ((size_t)HEAD + BODY) + 4 * sizeof(uint64_t);
   static_assert(NS % 2 == 0, "2x2 tiling needs an even number of scalar dofs");
   static_assert(CELLS * (NTILE + 1) <= ACC, "one (cell, tile) per accumulating thread");
+  static_assert(!WARP_CELLS || (WCELLS * (ACC / 32) == CELLS && WCELLS * NTILE <= 32),
+                "ws: warp-owned cells");
   static_assert((CSTRIDE / 2) % 2 == 1, "conflict-free staging stride");
   static_assert(HEAD % 2 == 0 && REC_DBL % 2 == 0, "16-byte aligned buffers");
 };
@@ -105,12 +123,36 @@ struct PairSlot {
   int cell, j0, k0;
   bool active, diag;
 };
+// ws lane -> (cell of the warp) * 16 + tile for NS = 10, 2 cells per warp and a
+// staging cell stride of 902 doubles: the 16-byte staging stores of every quarter-warp
+// hit distinct bank groups, and of the whole warp at most ceil(bytes / 128) per group
+// (direct and mirrored; searched offline; -1 idle)
+__constant__ signed char c_ws_lane10[32] = {7,  6,  17, 9,  18, 2,  16, 30, 14, 5,  24,
+                                            13, 22, 1,  8,  11, 29, 4,  20, 28, 26, 12,
+                                            19, 3,  10, 27, 25, 23, 21, 0,  -1, -1};
+
+// flat kernel: cell = tid % CELLS (a warp spans all cells of the tile);
+// ws kernel: warp w owns cells WCELLS*w .. WCELLS*w + WCELLS-1 (one lane per (cell, tile)),
+// so a warp stages and stores its cells without waiting for the other warps
 template <class Sh>
 __device__ __forceinline__ PairSlot pair_slot(int tid) {
   PairSlot s;
-  s.cell = tid % Sh::CELLS;
-  const int my_tile = tid / Sh::CELLS;
-  s.active = my_tile < Sh::NTILE;
+  int my_tile;
+  if constexpr (Sh::WARP_CELLS && Sh::NJ == 5 && Sh::WCELLS == 2 && Sh::CSTRIDE % 16 == 6) {
+    const int code = c_ws_lane10[tid & 31];
+    s.cell = (tid >> 5) * Sh::WCELLS + (code >= 0 ? code >> 4 : 0);
+    my_tile = code & 15;
+    s.active = code >= 0;
+  } else if constexpr (Sh::WARP_CELLS) {
+    const int lane = tid & 31;
+    s.cell = (tid >> 5) * Sh::WCELLS + lane / Sh::NTILE;
+    my_tile = lane % Sh::NTILE;
+    s.active = lane < Sh::WCELLS * Sh::NTILE;
+  } else {
+    s.cell = tid % Sh::CELLS;
+    my_tile = tid / Sh::CELLS;
+    s.active = my_tile < Sh::NTILE;
+  }
   int TJ = 0, TK = 0, t = s.active ? my_tile : 0;
   for (int J = 0; J < Sh::NJ; ++J) {
     const int len = Sh::NJ - J;
@@ -239,9 +281,13 @@ __device__ __forceinline__ void pair_stage(double* stg, const double (&a4)[2][2]
     for (int c = 0; c < 3; ++c)
 #pragma unroll
       for (int d = 0; d < 3; ++d)
-        // row (c, j0+x), columns (d, k0..k0+1): one 16-byte store
+        // row (c, j0+x), columns (d, k0..k0+1): one 16-byte store.  Diagonal tile:
+        // entry (j0+1, k0) is the mirror of (j0, k0+1) (the lower triangle is the
+        // mirrored upper one) -- folded into this store (ws), or stored apart (flat:
+        // measured faster there)
         *reinterpret_cast<double2*>(&stg[(c * NS + sl.j0 + x) * N + d * NS + sl.k0]) =
-            make_double2(a4[x][0][c][d], a4[x][1][c][d]);
+            make_double2(Sh::WARP_CELLS && x == 1 && sl.diag ? a4[0][1][d][c] : a4[x][0][c][d],
+                         a4[x][1][c][d]);
   if (!sl.diag) {
 #pragma unroll
     for (int y = 0; y < 2; ++y)
@@ -252,8 +298,7 @@ __device__ __forceinline__ void pair_stage(double* stg, const double (&a4)[2][2]
           // mirror: row (d, k0+y), columns (c, j0..j0+1)
           *reinterpret_cast<double2*>(&stg[(d * NS + sl.k0 + y) * N + c * NS + sl.j0]) =
               make_double2(a4[0][y][c][d], a4[1][y][c][d]);
-  } else {
-    // diagonal tile: entry (j0+1, k0) is the mirror of (j0, k0+1)
+  } else if constexpr (!Sh::WARP_CELLS) {
 #pragma unroll
     for (int c = 0; c < 3; ++c)
 #pragma unroll
@@ -337,23 +382,39 @@ __global__ void __launch_bounds__(PairShape<FEMGPU_ELASTICITY, NS, Q>::THREADS, 
       mbar_wait(&full[b], (uint32_t)((it >> 1) & 1));
       const double* rec = sRec + b * Sh::REC_DBL;
       const double* qsb = rec + Q * NS * Sh::JS;
-      if (sl.active) {
-#pragma unroll 1
+      if (sl.active && !(PAIR_ABL & 1)) {
+#pragma unroll kPairWsQUnroll
         for (int q = 0; q < Q; ++q)
           pair_point<Sh>(a4, t1, rec + q * NS * Sh::JS + sl.cell,
                          qsb + q * Sh::QSD * CELLS + sl.cell, sl.j0, sl.k0);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive_cta(&empty[b]);
-      if (tid == 0) bulk_wait_read0();  // previous tile's bulk stores have read the staging
-      named_bar(1, Sh::ACC);
+      // this warp's cells only: its previous bulk stores have read its staging rows
+      if (lane == 0) bulk_wait_read0();
+      __syncwarp();
       add_t1(a4, t1);
-      if (sl.active) pair_stage<Sh>(sStg + sl.cell * Sh::CSTRIDE, a4, sl);
+      if (sl.active && !(PAIR_ABL & 16)) pair_stage<Sh>(sStg + sl.cell * Sh::CSTRIDE, a4, sl);
+      if ((PAIR_ABL & 16) && sl.active) {  // keep the accumulate alive: one value per thread
+        double sum = 0;
+        for (int i = 0; i < 36; ++i) sum += (&a4[0][0][0][0])[i];
+        sStg[sl.cell * Sh::CSTRIDE + lane % Sh::NTILE] = sum;
+      }
       fence_proxy_async();
-      named_bar(1, Sh::ACC);
-      if (tid == 0) pair_bulk_store<Sh>(A, c0, nt, sStg, acc);
+      __syncwarp();
+      if (lane == 0 && !(PAIR_ABL & 2)) {
+        const int cw = (tid >> 5) * Sh::WCELLS;
+        for (int c = cw; c < min(cw + Sh::WCELLS, nt); ++c) {
+          double* dst = A + (c0 + c) * (size_t)Sh::N * Sh::N;
+          if (acc)
+            bulk_s2g_add(dst, sStg + c * Sh::CSTRIDE, Sh::N * Sh::N * 8);
+          else
+            bulk_s2g(dst, sStg + c * Sh::CSTRIDE, Sh::N * Sh::N * 8);
+        }
+        bulk_commit();
+      }
     }
-    if (tid == 0) bulk_wait0();
+    if (lane == 0) bulk_wait0();
   } else {
     // ---------------- producers: inputs (cp.async, one tile ahead), geometry, records ----
     const int pt = tid - Sh::ACC;
@@ -363,7 +424,7 @@ __global__ void __launch_bounds__(PairShape<FEMGPU_ELASTICITY, NS, Q>::THREADS, 
       double* in = sIn + (it & 1) * Sh::IN_DBL;
       for (int i = pt; i < nt * 12; i += Sh::PROD) cp_async8(&in[i], coords + c0 * 12 + i);
       for (int i = pt; i < nt * Sh::NCOEF; i += Sh::PROD)
-        cp_async8(&in[CELLS * 12 + i], coef + c0 * Sh::NCOEF + i);
+        cp_async8(&in[CELLS * 12 + (i / Sh::NCOEF) * Sh::CF + i % Sh::NCOEF], coef + c0 * Sh::NCOEF + i);
       asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
     prefetch(0);
@@ -379,7 +440,7 @@ __global__ void __launch_bounds__(PairShape<FEMGPU_ELASTICITY, NS, Q>::THREADS, 
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
       }
       named_bar(2, Sh::PROD);
-      if (pt < CELLS) {
+      if (pt < CELLS && !(PAIR_ABL & 8)) {
         double x[12];
 #pragma unroll
         for (int r = 0; r < 12; ++r)  // cells past the end: reference tet (never stored)
@@ -397,13 +458,16 @@ __global__ void __launch_bounds__(PairShape<FEMGPU_ELASTICITY, NS, Q>::THREADS, 
       double* rec = sRec + b * Sh::REC_DBL;
       double* qsb = rec + Q * NS * Sh::JS;
       // thread -> (cell, q): K, mu', lam' once, then the 10 records g_j = K^T D phi_j
-      for (int task = pt; task < CELLS * Q; task += Sh::PROD) {
-        const int c = task % CELLS, q = task / CELLS;
+      for (int task = pt; task < ((PAIR_ABL & 4) ? 0 : CELLS * Q); task += Sh::PROD) {
+        // q, q + Q/2 share a half-warp: their record rows start NS*JS*Q/2 doubles apart,
+        // opposite bank halves for the c3 shape (conflict-free 8-byte record stores)
+        const int c = task % CELLS, r = task / CELLS;
+        const int q = (Q % 2 == 0) ? (r & 1) * (Q / 2) + (r >> 1) : r;
         const double* Kp = sCell + c * Sh::CELLD;
         double K[9];
 #pragma unroll
         for (int i = 0; i < 9; ++i) K[i] = Kp[i];
-        const double* cf = in + CELLS * 12 + c * Sh::NCOEF;
+        const double* cf = in + CELLS * 12 + c * Sh::CF;
         double muq = 0, lamq = 0;
         if (c < nt) {
 #pragma unroll
