@@ -47,6 +47,9 @@
 #ifndef PAIR_WS_QUNROLL
 #define PAIR_WS_QUNROLL 8  // elasticity consumers (Q = 8; measured 1.081 -> 1.011 ms on c3 vs 1)
 #endif
+#ifndef PAIR_FLAT_WARP_CELLS
+#define PAIR_FLAT_WARP_CELLS 0  // warp-owned cells in the flat (SVK) kernel: 1.48 vs 1.42 ms on c4
+#endif
 #ifndef PAIR_ELAS_FLAT
 #define PAIR_ELAS_FLAT 0
 #endif
@@ -78,7 +81,7 @@ struct PairShape {
   static constexpr int RECD = SVK ? 9 : 3;               // per (q,j): g | h | s
   static constexpr int QSD = SVK ? 8 : 2;                // per q: lam', mu' | F F^T (6)
   // ws (elasticity): each warp owns WCELLS cells of the tile (see pair_slot)
-  static constexpr bool WARP_CELLS = !FLAT;
+  static constexpr bool WARP_CELLS = !FLAT || PAIR_FLAT_WARP_CELLS;
   static constexpr int WCELLS = CELLS / (ACC / 32);
   // j-stride of a record buffer.  flat: RECD*CELLS + 4 doubles, so the k-side loads
   // of the (j,k) tiles sharing a warp (k0 two apart) fall in alternate bank halves;
@@ -93,7 +96,7 @@ struct PairShape {
   static constexpr int CELLD = 10;                       // K(9), adet
   // ws: coefficient rows padded to an odd stride (the producer's per-(cell, q) reads
   // of 8 cells' rows are conflict-free)
-  static constexpr int CF = WARP_CELLS ? NCOEF + 1 : NCOEF;
+  static constexpr int CF = !FLAT ? NCOEF + 1 : NCOEF;
   static constexpr int IN_DBL = CELLS * (12 + CF);       // raw inputs
   static constexpr int HEAD = TAB + CELLS * CELLD + (FLAT ? 1 : 2) * IN_DBL;  // ws: double-buffered inputs
   // ws: two record buffers + separate staging; flat: one record buffer aliasing staging
