@@ -564,8 +564,14 @@ __global__ void __launch_bounds__(128, 2)
       const int qn = min(Sh::QC, Q - q0);
       // ---- per (cell, q), one thread: F = I + grad w, E, w'S, F F^T, lam', mu',
       //      then the 10 records g_j, h_j = F g_j, s_j = w' S g_j (F, S in registers)
-      for (int task = tid; task < CELLS * qn; task += Sh::THREADS) {
-        const int c = task % CELLS, ql = task / CELLS, q = q0 + ql;
+      // warp-owned cells (JS odd): q and q + 4 share a half-warp, so the record
+      // stores of its 16 lanes fall in opposite bank halves
+      constexpr int NTASK = Sh::WARP_CELLS ? CELLS * ((Sh::QC + 7) / 8 * 8) : CELLS * Sh::QC;
+      for (int task = tid; task < NTASK; task += Sh::THREADS) {
+        const int c = task % CELLS, r = task / CELLS;
+        const int ql = Sh::WARP_CELLS ? (r >> 3) * 8 + (r & 1) * 4 + ((r & 7) >> 1) : r;
+        if (ql >= qn) continue;
+        const int q = q0 + ql;
         const double* K = sCell + c * Sh::CELLD;
         constexpr int CO = Sh::SVK ? 3 * NS : 0;  // offset of mu, lam in the dofs
         double muq = 0, lamq = 0;
