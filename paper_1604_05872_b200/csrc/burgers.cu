@@ -47,6 +47,10 @@
 
 namespace femgpu {
 
+#ifndef BZ_RING_LA
+#define BZ_RING_LA 8  // R2 stages in flight ahead of the consuming k4 step
+#endif
+
 namespace bz {
 constexpr int NS = 20;
 constexpr int N = 60;
@@ -75,6 +79,7 @@ constexpr int CELLD = 10;                     // K(9), adet
 constexpr int NPAIR = 25;                     // GEMM-2 B tile pairs: 15 direct + 10 mirror
 constexpr int STAGE_DBL = NPAIR * 64;         // one k4 step of R2
 constexpr int NRING = 8;                      // ring stages (alias slabs 0 and 1)
+constexpr int RING_LA = BZ_RING_LA < NRING ? BZ_RING_LA : NRING;  // stages in flight
 constexpr size_t SMEM =
     sizeof(double) * (size_t)(NSLAB * SLAB_DBL + DN_DBL + 2 * A1_DBL + 2 * A2_DBL + IN_DBL +
                               CELLS * CELLD) + 8 * (1 + 2 * 8 + 2 * 3);
@@ -164,7 +169,7 @@ __device__ __forceinline__ void nbar_arrive(int id, int n) {
 
 #ifdef BZ_TRACE
 // development trace (CTA 0 only): clock64 at pipeline milestones per tile
-__device__ unsigned long long bz_trace[128][16];
+__device__ unsigned long long bz_trace[128][20];
 #define BZ_MARK(it, slot, cond) \
   if (blockIdx.x == 0 && (cond) && (it) < 128) bz_trace[it][slot] = clock64()
 #define BZ_T0() const unsigned long long bz_t0 = clock64()
@@ -376,7 +381,7 @@ __global__ void __launch_bounds__(bz::THREADS, 1)
     bulk_g2s(sRing + slot * STAGE_DBL, gR2 + (size_t)ks * STAGE_DBL, STAGE_DBL * 8, &rFull[slot]);
   };
   if (issuer && my_tiles > 0)
-    for (int ks = 0; ks < NRING; ++ks) ring_issue(ks);
+    for (int ks = 0; ks < RING_LA; ++ks) ring_issue(ks);
 
   long gi = 0;  // running (c,d) block counter of this CTA: slab gi % NSLAB
   for (long it = 0; it < my_tiles; ++it) {
@@ -398,6 +403,8 @@ __global__ void __launch_bounds__(bz::THREADS, 1)
       const long G = it * KS2 + ks;
       const int slot = (int)(G % NRING);
       mbar_wait(&rFull[slot], (uint32_t)((G / NRING) & 1));
+      BZ_MARK(it, 16, tid == 0 && ks == 0);
+      BZ_MARK(it, 19, tid == 0 && ks == KS2 - 1);
       const double2* st = reinterpret_cast<const double2*>(sRing + slot * STAGE_DBL);
       const double2 bd = st[pdir * 32 + lane];
       const double2 bm = mirror ? st[pmir * 32 + lane] : make_double2(0.0, 0.0);
@@ -410,9 +417,10 @@ __global__ void __launch_bounds__(bz::THREADS, 1)
         dmma16x8x4(cmir[0], af.x, af.y, bm.x);
         dmma16x8x4(cmir[1], af.x, af.y, bm.y);
       }
-      if (issuer && ks + NRING < KS2) {  // refill the slot with stage ks + NRING
-        mbar_wait(&rEmpty[slot], (uint32_t)((G / NRING) & 1));
-        ring_issue(G + NRING);
+      if (issuer && ks + RING_LA < KS2) {  // stage ks + RING_LA into its slot
+        const long G2 = G + RING_LA;
+        if (G2 >= NRING) mbar_wait(&rEmpty[G2 % NRING], (uint32_t)(((G2 / NRING) - 1) & 1));
+        ring_issue(G2);
       }
     }
     BZ_MARK(it, 5, tid == 0);
@@ -508,8 +516,10 @@ __global__ void __launch_bounds__(bz::THREADS, 1)
     }
     if (issuer && it + 1 < my_tiles) {
       // slabs 0 and 1 (stores of steps 6, 7) read out -> first stages of the next tile
+      BZ_MARK(it, 17, true);
       bulk_wait_read1();
-      for (int k = 0; k < NRING; ++k) {
+      BZ_MARK(it, 18, true);
+      for (int k = 0; k < RING_LA; ++k) {
         const long G = (it + 1) * KS2 + k;
         mbar_wait(&rEmpty[G % NRING], (uint32_t)(((G / NRING) - 1) & 1));
         ring_issue(G);

@@ -29,9 +29,9 @@ for _ in range(3):
     form.assemble(x, c, out)
 torch.cuda.synchronize()
 L = femgpu.lib()
-buf = (C.c_ulonglong * (128 * 16))()
+buf = (C.c_ulonglong * (128 * 20))()
 L.femgpu_debug_trace(buf)
-T = np.array(buf, dtype=np.float64).reshape(128, 16)
+T = np.array(buf, dtype=np.float64).reshape(128, 20)
 ntile = int((T[:, 4] > 0).sum())
 t0 = T[0, 0]
 print(f"tiles traced {ntile}")
@@ -45,3 +45,7 @@ per_tile = np.diff(T[:ntile, 4])
 print(f"mean tile period (kcycles) {per_tile[2:].mean()/1e3:.2f}; gemm2 {np.mean(T[2:ntile,5]-T[2:ntile,4])/1e3:.2f};"
       f" steps {np.mean(T[2:ntile,14]-T[2:ntile,5])/1e3:.2f}; producer A1 {np.mean(T[2:ntile,2]-T[2:ntile,1])/1e3:.2f},"
       f" A2 {np.mean(T[2:ntile,3]-T[2:ntile,2])/1e3:.2f}; issuer wait {np.mean(T[2:ntile,15])/1e3:.2f}")
+print("ring (per tile, kcycles after compFull): first stage landed, last stage landed; issuer at tile end: wait_read1 start/end (after the tile's last step)")
+for it in range(2, min(ntile, 10)):
+    r = T[it]
+    print(f"{it:3d} first {(r[16]-r[4])/1e3:6.2f} last {(r[19]-r[4])/1e3:6.2f} gemm2 {(r[5]-r[4])/1e3:6.2f} | wait_read1 {(r[17]-r[14])/1e3:6.2f} -> {(r[18]-r[14])/1e3:6.2f}  next compFull {(T[it+1][4]-r[14])/1e3:6.2f}")
