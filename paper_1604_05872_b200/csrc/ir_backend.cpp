@@ -9,7 +9,7 @@
 //
 //   * maps the order-free element loop onto the grid -- one thread per cell, or
 //     one warp per cell with the output rows spread over the lanes and
-//     accumulated in registers (chosen by an op-count model; both exact);
+//     accumulated in registers (warp whenever the row loop has >= 8 rows; both exact);
 //   * prints every expression exactly as emit_c prints it (precedence-driven,
 //     nested sums and products flattened, emit_c.cpp:47-80) and is compiled
 //     with --fmad=false, so it performs femopt's emitted arithmetic operation
@@ -328,6 +328,17 @@ struct Emitter {
   std::map<std::string, long> rest;
   std::set<std::string> acc_dims;
   std::vector<std::string> lines;
+  // warp mapping: loops outside the row loop whose iterations fill per-index
+  // array temporaries are spread over the lanes; those arrays live in shared
+  // memory (one row per warp) and are read by every lane
+  std::set<const Node*> dist;
+  std::set<std::string> shared;
+  bool in_J = false;
+
+  std::string temp_ref(const std::string& name, const std::string& flat) const {
+    if (shared.count(name)) return "s_" + ident(name) + "[w_][" + flat + "]";
+    return "v_" + ident(name) + "[" + flat + "]";
+  }
 
   std::string ext_of(const std::string& d) const {
     return d == e_index ? std::string("E") : std::to_string(ext.at(d));
@@ -368,7 +379,7 @@ struct Emitter {
       std::vector<std::string> idx;
       for (size_t i = 2; i < x.arr.size(); ++i) idx.push_back(x.arr[i].str);
       if (tabs.count(name)) return "t_" + ident(name) + "[" + offset(name, idx) + "]";
-      if (temps.count(name)) return "v_" + ident(name) + "[" + temp_flat(name, idx) + "]";
+      if (temps.count(name)) return temp_ref(name, temp_flat(name, idx));
       if (outs.count(name)) return "o_" + ident(name) + "[" + offset(name, idx) + "]";
       irfail("unknown array '" + name + "'");
     }
@@ -409,9 +420,24 @@ struct Emitter {
           lines.push_back(pad + "for (int r_ = 0; r_ < " + std::to_string(R) + "; ++r_) {");
           lines.push_back(pad + "  const int i_" + ident(J) + " = lane_ + 32 * r_;");
           lines.push_back(pad + "  if (i_" + J + " < " + std::to_string(n.end) + ") {");
+          in_J = true;
+          emit_nodes(n.body, ind + 2);
+          in_J = false;
+          lines.push_back(pad + "  }");
+          lines.push_back(pad + "}");
+          continue;
+        }
+        if (warp && !in_J && dist.count(&n)) {
+          const long cnt = std::max<long>(0, n.end - n.begin);
+          lines.push_back(pad + "__syncwarp();");
+          lines.push_back(pad + "for (int d_ = 0; d_ < " + std::to_string((cnt + 31) / 32) + "; ++d_) {");
+          lines.push_back(pad + "  const int i_" + ident(n.index) + " = " + std::to_string(n.begin) +
+                          " + lane_ + 32 * d_;");
+          lines.push_back(pad + "  if (i_" + n.index + " < " + std::to_string(n.end) + ") {");
           emit_nodes(n.body, ind + 2);
           lines.push_back(pad + "  }");
           lines.push_back(pad + "}");
+          lines.push_back(pad + "__syncwarp();");
           continue;
         }
         if (warp && n.end - n.begin <= 64 && acc_dims.count(n.index)) {
@@ -434,7 +460,7 @@ struct Emitter {
         } else if (outs.count(n.name)) {
           target = "o_" + n.name + "[" + offset(n.name, n.idx) + "]";
         } else if (!temps.at(n.name).empty()) {
-          target = "v_" + n.name + "[" + temp_flat(n.name, n.idx) + "]";
+          target = temp_ref(n.name, temp_flat(n.name, n.idx));
         } else {
           target = "v_" + n.name;
         }
@@ -512,6 +538,89 @@ bool warp_plan(const std::vector<Node>& tree, Emitter& em) {
   return ok;
 }
 
+void refs(const std::vector<Node>& ns, const Node* skip, std::set<std::string>& acc) {
+  for (const Node& n : ns) {
+    if (&n == skip) continue;
+    if (n.loop) {
+      refs(n.body, skip, acc);
+    } else {
+      acc.insert(n.name);
+      names_in(*n.rhs, acc);
+    }
+  }
+}
+
+// Loops of the element body, outside the row loop J, that can run lane-parallel
+// in the warp mapping: statements only (no nested loops), each writing either an
+// array temporary subscripted by exactly the loop index, or a scalar temporary
+// used nowhere else; no outputs.  Such an array is shared (one copy per warp)
+// when every write of it is in such a loop.
+void plan_distribution(const std::vector<Node>& body, Emitter& em) {
+  std::vector<const Node*> cand;
+  std::function<void(const std::vector<Node>&)> find = [&](const std::vector<Node>& ns) {
+    for (const Node& n : ns) {
+      if (!n.loop || n.index == em.J) continue;
+      bool flat = true;
+      for (const Node& c : n.body) flat = flat && !c.loop;
+      if (!flat) {
+        find(n.body);
+        continue;
+      }
+      std::set<std::string> outside;
+      refs(body, &n, outside);
+      bool ok = n.end > n.begin;
+      for (const Node& c : n.body) {
+        std::set<std::string> used;
+        names_in(*c.rhs, used);
+        for (const auto& o : em.outs)
+          if (used.count(o)) ok = false;
+        if (em.outs.count(c.name) || !em.temps.count(c.name)) {
+          ok = false;
+        } else if (em.temps.at(c.name).empty()) {
+          if (outside.count(c.name)) ok = false;
+        } else if (em.temps.at(c.name) != std::vector<std::string>{n.index} ||
+                   c.idx != std::vector<std::string>{n.index}) {
+          ok = false;
+        }
+      }
+      if (ok) cand.push_back(&n);
+    }
+  };
+  find(body);
+  // writes of each array temporary: all of them / inside candidate loops
+  std::map<std::string, int> all_w;
+  std::function<void(const std::vector<Node>&)> count = [&](const std::vector<Node>& ns) {
+    for (const Node& n : ns) {
+      if (n.loop) count(n.body);
+      else if (em.temps.count(n.name) && !em.temps.at(n.name).empty()) ++all_w[n.name];
+    }
+  };
+  count(body);
+  for (bool changed = true; changed;) {
+    changed = false;
+    std::map<std::string, int> in_w;
+    for (const Node* L : cand)
+      for (const Node& c : L->body)
+        if (!em.temps.at(c.name).empty()) ++in_w[c.name];
+    for (auto it = cand.begin(); it != cand.end();) {
+      bool keep = true;
+      for (const Node& c : (*it)->body)
+        if (!em.temps.at(c.name).empty() && in_w[c.name] != all_w[c.name]) keep = false;
+      if (keep) {
+        ++it;
+      } else {
+        it = cand.erase(it);
+        changed = true;
+      }
+    }
+  }
+  for (const Node* L : cand) {
+    em.dist.insert(L);
+    for (const Node& c : L->body)
+      if (!em.temps.at(c.name).empty()) em.shared.insert(c.name);
+  }
+}
+
 void scan(const std::vector<Node>& nodes, Emitter& em) {
   for (const Node& n : nodes) {
     if (n.loop) {
@@ -569,11 +678,13 @@ std::unique_ptr<Kernel> generate(const char* json, int strategy) {
   const bool can_warp = warp_plan(tree, em);
   bool warp = false;
   if (strategy == 0) {
-    if (can_warp && em.ext.at(em.J) >= 8) {
-      double t[2] = {0, 0};
-      op_counts(tree, 1, false, em.J, t);
-      warp = 31 * t[0] < 0.25 * t[1];
-    }
+    // warp per cell whenever a row loop of >= 8 rows exists: its register
+    // accumulators replace the thread mapping's per-statement global += (which
+    // femopt's optimized nests put inside the quadrature loop) and spread the
+    // j-loop over lanes.  Measured on the BASELINE forms (profiles/
+    // bench_generic_r01.jsonl): warp 1.1-42x faster for n >= 20, raw and
+    // optimized alike; thread 2-12x faster for n = 4 (P1), where 28 lanes idle.
+    warp = can_warp && em.ext.at(em.J) >= 8;
   } else if (strategy == 2) {
     if (!can_warp) irfail("the warp mapping does not apply to this nest");
     warp = true;
@@ -614,8 +725,10 @@ std::unique_ptr<Kernel> generate(const char* json, int strategy) {
     if (!n.loop && em.outs.count(n.name)) irfail("output written outside the element loop");
   em.emit_nodes(pre, 1);
   if (warp) {
+    plan_distribution(body, em);
     em.lines.push_back("  const long i_" + em.e_index + " = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;");
     em.lines.push_back("  const int lane_ = threadIdx.x & 31;");
+    if (!em.shared.empty()) em.lines.push_back("  const int w_ = threadIdx.x >> 5;");
     em.lines.push_back("  if (i_" + em.e_index + " >= E) return;");
     for (const auto& o : em.outs) {
       const std::string n = std::to_string(em.R * em.rest[o]);
@@ -670,7 +783,10 @@ std::unique_ptr<Kernel> generate(const char* json, int strategy) {
         if (d == em.e_index) irfail("temporary " + kv.first + " indexed by the element loop");
         n *= em.ext.at(d);
       }
-      src += "  double v_" + ident(kv.first) + "[" + std::to_string(n) + "];\n";
+      if (em.shared.count(kv.first))
+        src += "  __shared__ double s_" + ident(kv.first) + "[4][" + std::to_string(n) + "];\n";
+      else
+        src += "  double v_" + ident(kv.first) + "[" + std::to_string(n) + "];\n";
     } else {
       src += "  double v_" + ident(kv.first) + ";\n";
     }

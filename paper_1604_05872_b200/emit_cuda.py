@@ -11,7 +11,7 @@ NVRTC for sm_100a:
 
   * the order-free element loop becomes the grid: one thread per cell, or one
     warp per cell with the output rows over the lanes and register
-    accumulators (chosen by an op-count model);
+    accumulators (warp whenever the row loop has >= 8 rows: measured faster);
   * expressions are printed exactly as emit_c prints them and compiled without
     FMA contraction, so the results are bit-identical to femopt's emitted C
     (``-ffp-contract=off``) on the same inputs;

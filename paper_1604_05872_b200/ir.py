@@ -496,5 +496,29 @@ def argument_order(ir: dict):
     return outs, tabs, consts
 
 
+def e_tables(cfg, coords, coeffs) -> dict:
+    """The per-cell (SoA, ``name[e]``) input tables of this module's IR for a whole
+    mesh, from cell-major coords ``[E][4][3]`` and coefficients ``[E][ncoef]``:
+    what a caller supplies at run time to a kernel built on a few cells."""
+    coords = np.asarray(coords, dtype=np.float64)
+    coeffs = np.asarray(coeffs, dtype=np.float64)
+    E = coords.shape[0]
+    x = coords.reshape(E, 4, 3)
+    t = {f"x{v}{c}": x[:, v, c] for v in range(4) for c in range(3)}
+    ns = cfg.ns
+    if cfg.kind == fe.HELMHOLTZ:
+        t.update({f"f{m:02d}": coeffs[:, m] for m in range(coeffs.shape[1])})
+    elif cfg.kind == fe.ELASTICITY:
+        t.update({f"mu{m}": coeffs[:, m] for m in range(4)})
+        t.update({f"lam{m}": coeffs[:, 4 + m] for m in range(4)})
+    elif cfg.kind == fe.HYPERELASTICITY:
+        t.update({f"w{c}{m:02d}": coeffs[:, c * ns + m] for c in range(3) for m in range(ns)})
+        t.update({f"mu{m}": coeffs[:, 3 * ns + m] for m in range(4)})
+        t.update({f"lam{m}": coeffs[:, 3 * ns + 4 + m] for m in range(4)})
+    else:
+        t.update({f"u{c}{m:02d}": coeffs[:, c * ns + m] for c in range(3) for m in range(ns)})
+    return {k: np.ascontiguousarray(v) for k, v in t.items()}
+
+
 def dumps(ir: dict) -> str:
     return json.dumps(ir, separators=(",", ":"))

@@ -161,3 +161,66 @@ def test_residual_derivative_is_the_jacobian(name):
     Jd = np.einsum("ejk,ek->ej", out.cpu().numpy(), delta)
     rel = np.linalg.norm(fd - Jd, axis=1) / np.linalg.norm(Jd, axis=1)
     assert rel.max() < 1e-7, rel
+
+
+# ----------------------------------------------------------------------------
+# femopt's own optimized kernels of the BASELINE configs (oracle/make_ir_full.py)
+IR_FULL = os.path.join(os.path.dirname(__file__), "golden", "ir_full")
+FULL_CASES = sorted(f[:-len(".json.gz")] for f in os.listdir(IR_FULL)) if os.path.isdir(IR_FULL) else []
+
+
+def _load_full(case):
+    import gzip
+
+    with gzip.open(os.path.join(IR_FULL, case + ".json.gz"), "rt") as f:
+        return json.load(f)
+
+
+def test_full_config_ir_fixtures():
+    # every config has femopt's optimized kernels for each reference-arm plan
+    assert {c.split("_")[0] for c in FULL_CASES} >= {"c1", "c2", "c3", "c4", "c5"}
+    for case in FULL_CASES:
+        d = _load_full(case)
+        cfg = fe.CONFIGS[d["config"]]
+        outs = [k["output"] for k in d["kernels"]]
+        assert outs == (["A"] if cfg.kind != fe.BURGERS else
+                        [f"A{c}{e}" for c in range(3) for e in range(3)])
+        for k in d["kernels"]:
+            assert k["flops_per_cell"] <= k["flops_raw_per_cell"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", FULL_CASES)
+def test_femopt_optimized_kernel_on_gpu_matches_fast_path(case):
+    # femopt's optimized kernel of a BASELINE config, run by the generic backend
+    # on fresh cells (e-tables at run time), against the hand-written kernel
+    torch = pytest.importorskip("torch")
+    from paper_1604_05872_b200 import femgpu
+
+    d = _load_full(case)
+    cfg = fe.CONFIGS[d["config"]]
+    E = 333
+    coords, coeffs = fe.cell_inputs(cfg, ncells=E)
+    dev = torch.device("cuda:0")
+    et = {k: torch.from_numpy(v).to(dev) for k, v in ir.e_tables(cfg, coords, coeffs).items()}
+    got = np.zeros((E, cfg.n, cfg.n))
+    for kk in d["kernels"]:
+        k = kk["ir"]
+        K = emit_cuda.IRKernel(k)
+        inputs = {n: et[n] if n in et else torch.tensor(np.asarray(k["tables"][n]["values"]),
+                                                        device=dev) for n in K.inputs}
+        (o,) = K.outputs
+        out = torch.zeros(K.size(0, o, E), dtype=torch.float64, device=dev)
+        K.run({o: out}, inputs, k.get("constants", {}), E)
+        blk = out.cpu().numpy()
+        if o == "A":
+            got[:] = blk.reshape(E, cfg.n, cfg.n)
+        else:
+            c, e, ns = int(o[1]), int(o[2]), cfg.ns
+            got[:, c * ns:(c + 1) * ns, e * ns:(e + 1) * ns] = blk.reshape(E, ns, ns)
+    ref = torch.empty((E, cfg.n, cfg.n), dtype=torch.float64, device=dev)
+    femgpu.Form.from_config(cfg).assemble(torch.from_numpy(coords).to(dev),
+                                          torch.from_numpy(coeffs).to(dev), ref)
+    A = ref.cpu().numpy()
+    rel = np.linalg.norm((got - A).reshape(E, -1), axis=1) / np.linalg.norm(A.reshape(E, -1), axis=1)
+    assert rel.max() < 1e-12

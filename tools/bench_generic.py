@@ -1,77 +1,101 @@
 #!/usr/bin/env python3
-"""Throughput of the generic IR backend (emit_cuda) on the BASELINE meshes.
+"""Throughput of the generic IR backend (femgpu_ir_*, emit_cuda.py) on the BASELINE meshes.
 
-The raw femopt IR of each config (ir.py, built on 4 cells for its code) is
-compiled by emit_cuda and run on the full config mesh with the per-cell
-e-tables supplied at run time; device-timed with CUDA events.  The hand-written
-kernels (bench.py) are the fast path; this is the thread-per-cell generic one.
-usage: bench_generic.py [cfg ...]"""
+Two IR sources per config:
+  * raw      -- the config's IR as ir.py writes it (built on 4 cells for its code);
+  * femopt   -- femopt's own optimized kernels of every plan the reference arm
+                times (tests/golden/ir_full/<cfg>_<plan>.json.gz, made by
+                oracle/make_ir_full.py): what a femopt user hands to a backend.
+The per-cell e-tables of the full mesh are supplied at run time; device-timed
+with CUDA events (median of 5 after a warm-up).  `ir_gflops` counts femopt's
+flop_count of the IR that runs (kernel.cpp:521) -- for the optimized plans that
+is the reference's F_alg, so the rate compares directly with the reference's
+CPU rate on the same kernel (bench.py --impl reference).  The hand-written
+kernels (bench.py) are the fast path.
+usage: bench_generic.py [--raw] [--femopt] [cfg ...]"""
+import argparse
+import gzip
 import json
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_1604_05872_b200 import emit_cuda, fe, ir  # noqa: E402
 
-
-def e_tables(cfg, coords, coeffs):
-    """SoA per-cell tables of ir.py's naming for the whole mesh."""
-    E = coords.shape[0]
-    x = coords.reshape(E, 4, 3)
-    t = {f"x{v}{c}": x[:, v, c] for v in range(4) for c in range(3)}
-    ns = cfg.ns
-    if cfg.kind == fe.HELMHOLTZ:
-        t.update({f"f{m:02d}": coeffs[:, m] for m in range(coeffs.shape[1])})
-    elif cfg.kind == fe.ELASTICITY:
-        t.update({f"mu{m}": coeffs[:, m] for m in range(4)})
-        t.update({f"lam{m}": coeffs[:, 4 + m] for m in range(4)})
-    elif cfg.kind == fe.HYPERELASTICITY:
-        t.update({f"w{c}{m:02d}": coeffs[:, c * ns + m] for c in range(3) for m in range(ns)})
-        t.update({f"mu{m}": coeffs[:, 3 * ns + m] for m in range(4)})
-        t.update({f"lam{m}": coeffs[:, 3 * ns + 4 + m] for m in range(4)})
-    else:
-        t.update({f"u{c}{m:02d}": coeffs[:, c * ns + m] for c in range(3) for m in range(ns)})
-    return t
+IR_FULL = os.path.join(ROOT, "tests", "golden", "ir_full")
 
 
-def main(names):
+def time_kernels(kernels, et, E, dev, strategy="auto"):
+    """kernels: list of IR dicts; returns (ms per pass over all kernels, strategies)."""
+    runs, strategies = [], []
+    for k in kernels:
+        K = emit_cuda.IRKernel(k, strategy)
+        strategies.append(K.strategy)
+        inputs = {n: et[n] if n in et else
+                  torch.tensor(np.asarray(k["tables"][n]["values"]), device=dev)
+                  for n in K.inputs}
+        outs = {o: torch.zeros(K.size(0, o, E), dtype=torch.float64, device=dev)
+                for o in K.outputs}
+        runs.append((K, outs, inputs, k.get("constants", {})))
+
+    def one():
+        for K, outs, inputs, consts in runs:
+            K.run(outs, inputs, consts, E)
+
+    one()
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        one()
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+    return sorted(times)[len(times) // 2], strategies
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--raw", action="store_true")
+    ap.add_argument("--femopt", action="store_true")
+    ap.add_argument("--strategy", default="auto", choices=["auto", "thread", "warp"])
+    ap.add_argument("configs", nargs="*", default=["c1", "c2", "c3", "c4", "c5"])
+    a = ap.parse_args()
+    if not (a.raw or a.femopt):
+        a.raw = a.femopt = True
     dev = torch.device("cuda:0")
-    for name in names:
+    for name in a.configs:
         cfg = fe.CONFIGS[name]
-        tabs = fe.tables(cfg)
-        c4, f4 = fe.cell_inputs(cfg, ncells=4)
-        kernels = ir.build(cfg, c4, f4, tabs=tabs)
         coords, coeffs = fe.cell_inputs(cfg)
         E = coords.shape[0]
-        et = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev)
-              for k, v in e_tables(cfg, coords, coeffs).items()}
-        total_ms = 0.0
-        for oname, k in kernels:
-            K = emit_cuda.IRKernel(k)
-            inputs = {}
-            for n in K.inputs:
-                if n in et:
-                    inputs[n] = et[n]
-                else:
-                    inputs[n] = torch.tensor(np.asarray(k["tables"][n]["values"]), device=dev)
-            outs = {o: torch.zeros(K.size(0, o, E), dtype=torch.float64, device=dev)
-                    for o in K.outputs}
-            K.run(outs, inputs, k.get("constants", {}), E)
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            reps = 3
-            e0.record()
-            for _ in range(reps):
-                K.run(outs, inputs, k.get("constants", {}), E)
-            e1.record()
-            torch.cuda.synchronize()
-            total_ms += e0.elapsed_time(e1) / reps
-        print(json.dumps({"config": name, "cells": E, "kernels": len(kernels), "ir": "raw (ufl)",
-                          "ms": round(total_ms, 3), "elem_per_s": E / (total_ms / 1e3)}), flush=True)
+        et = {k: torch.from_numpy(v).to(dev) for k, v in ir.e_tables(cfg, coords, coeffs).items()}
+        jobs = []
+        if a.raw:
+            tabs = fe.tables(cfg)
+            c4, f4 = fe.cell_inputs(cfg, ncells=4)
+            jobs.append(("raw (ufl)", [k for _, k in ir.build(cfg, c4, f4, tabs=tabs)], None))
+        if a.femopt:
+            for fn in sorted(os.listdir(IR_FULL)) if os.path.isdir(IR_FULL) else []:
+                if fn.startswith(name + "_") and fn.endswith(".json.gz"):
+                    with gzip.open(os.path.join(IR_FULL, fn), "rt") as f:
+                        d = json.load(f)
+                    jobs.append((f"femopt {d['plan']} ({d['encoding']})",
+                                 [k["ir"] for k in d["kernels"]], d["flops_per_cell"]))
+        for label, kernels, fpc in jobs:
+            ms, strategies = time_kernels(kernels, et, E, dev, a.strategy)
+            line = {"config": name, "cells": E, "ir": label, "kernels": len(kernels),
+                    "strategy": sorted(set(strategies)), "ms": round(ms, 3),
+                    "elem_per_s": E / (ms / 1e3)}
+            if fpc:
+                line["ir_flops_per_cell"] = fpc
+                line["ir_gflops"] = round(E * fpc / (ms / 1e3) / 1e9, 1)
+            print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["c1", "c2", "c3", "c4", "c5"])
+    main()
