@@ -32,9 +32,19 @@ namespace femgpu {
 // ============================================================================
 // P1: thread per cell, persistent CTAs, TMA bulk-copy input ring
 // ============================================================================
-constexpr int P1_TILE = 128;      // cells per tile = threads per CTA
-constexpr int P1_NBUF = 3;        // input stages in flight per CTA
-constexpr int P1_CTAS = 3;        // CTAs per SM
+#ifndef P1_TILE_CELLS
+#define P1_TILE_CELLS 128
+#endif
+#ifndef P1_STAGES
+#define P1_STAGES 2  // c1, 2000 launches from one CUDA graph (us per launch), tile x stages x
+                     // CTAs/SM: 128x2x2 62.8; 64x2x3 66.1; 64x4x2 67.0; 128x3x2 73.4; 128x3x3 73.6
+#endif
+#ifndef P1_CTAS_PER_SM
+#define P1_CTAS_PER_SM 2
+#endif
+constexpr int P1_TILE = P1_TILE_CELLS;  // cells per tile = threads per CTA
+constexpr int P1_NBUF = P1_STAGES;      // input stages in flight per CTA
+constexpr int P1_CTAS = P1_CTAS_PER_SM; // CTAs per SM
 constexpr int P1_SO = 18;         // padded output staging stride: conflict-free 16B stores
 constexpr int P1_IN = P1_TILE * 16;                       // doubles per input stage
 constexpr size_t P1_SMEM = sizeof(double) * (P1_NBUF * P1_IN + P1_TILE * P1_SO) +

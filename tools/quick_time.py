@@ -10,6 +10,7 @@ import torch  # noqa: E402
 
 from paper_1604_05872_b200 import fe, femgpu  # noqa: E402
 
+GRAPH = int(os.environ.get("QT_GRAPH", "0"))  # >0: time a graph of that many launches
 if os.environ.get("FEMGPU_LIB"):  # A/B builds (development)
     femgpu.LIB_PATH = os.environ["FEMGPU_LIB"]
 
@@ -34,12 +35,28 @@ def main(names):
         torch.cuda.synchronize()
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         times = []
-        for _ in range(10):
-            ev[0].record()
-            form.assemble(x, c, out)
-            ev[1].record()
-            torch.cuda.synchronize()
-            times.append(ev[0].elapsed_time(ev[1]) / 1e3)
+        if GRAPH:  # K launches back to back from one CUDA graph (bench.py's timing)
+            s = torch.cuda.Stream()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(s):
+                form.assemble(x, c, out, stream=s)
+                s.synchronize()
+                with torch.cuda.graph(g, stream=s):
+                    for _ in range(GRAPH):
+                        form.assemble(x, c, out, stream=s)
+            for _ in range(3):
+                ev[0].record()
+                g.replay()
+                ev[1].record()
+                torch.cuda.synchronize()
+                times.append(ev[0].elapsed_time(ev[1]) / 1e3 / GRAPH)
+        else:
+            for _ in range(10):
+                ev[0].record()
+                form.assemble(x, c, out)
+                ev[1].record()
+                torch.cuda.synchronize()
+                times.append(ev[0].elapsed_time(ev[1]) / 1e3)
         t = sorted(times)[len(times) // 2]
         bpc = cfg.bytes_per_cell()
         fpc = form.info["flops_per_cell"]
