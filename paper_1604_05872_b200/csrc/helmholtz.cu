@@ -198,15 +198,21 @@ cudaError_t launch_helm_p1(const HelmP1Params& prm, long E, const double* coords
 //                buffered) for the NEXT tile; mirrored, coalesced copy-out
 //   warp  12     TMA producer: S k-chunks into a 3-stage ring (bulk copies)
 // so the tensor cores never wait for a prologue or an epilogue.
+#ifndef HT_KPS
+#define HT_KPS 2
+#endif
+#ifndef HT_NBUF
+#define HT_NBUF 3
+#endif
 template <int NS, int NC>
 struct HelmTensorShape {
   static constexpr int NP = NS * (NS + 1) / 2;          // symmetric half of A_e
   static constexpr int NT = ((NP + 7) / 8 + 1) / 2 * 2;  // n8 tiles (even)
   static constexpr int KR = 7 * NC;                     // alpha = (m, s)
-  static constexpr int KPS = 2;                         // k8 steps per pipeline stage
+  static constexpr int KPS = HT_KPS;                    // k8 steps per pipeline stage
   static constexpr int KS = ((KR + 8 * KPS - 1) / (8 * KPS)) * KPS;  // k8 steps (padded)
   static constexpr int NSTG = KS / KPS;                 // stages per tile
-  static constexpr int NBUF = 3;                        // TMA ring depth
+  static constexpr int NBUF = HT_NBUF;                  // TMA ring depth
   static constexpr int MT = 2;                          // m16 tiles per CTA tile
   static constexpr int CELLS = 16 * MT;                 // cells per tile
   static constexpr int MMA_WARPS = 8;
