@@ -469,9 +469,13 @@ int femgpu_assemble_host(const femgpu_form* fc, long ncells, const double* coord
     if (!coords || !A || (f->ncoef > 0 && !coeffs)) throw Error(FEMGPU_ERR_INVALID_ARG, "null buffer");
     std::lock_guard<std::mutex> lock(f->host_mu);
     const size_t nn = (size_t)f->n * f->n;
-    // ~128 MiB of element matrices per chunk (multiple of 64 cells); three
+    // Chunks of at most ~128 MiB of element matrices and at most 1/8 of the
+    // call (so small element matrices still get a pipeline: c1's 1.6 M cells
+    // were 2 chunks), at least 8192 cells; multiples of 64 cells.  Three
     // streams rotate H2D -> kernel -> D2H so both copy engines stay busy.
-    const long chunk = std::max<long>(64, (long)((128u << 20) / (nn * 8)) / 64 * 64);
+    const long by_bytes = std::max<long>(64, (long)((128u << 20) / (nn * 8)) / 64 * 64);
+    const long by_count = std::max<long>(8192, (ncells / 8 + 63) / 64 * 64);
+    const long chunk = std::min(by_bytes, by_count);
     const size_t per_cell = 12 + f->ncoef + nn;
     if (f->host_chunk != chunk) {
       for (int i = 0; i < femgpu_form::NSTREAM; ++i) {
