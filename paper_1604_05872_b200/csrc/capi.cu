@@ -385,7 +385,7 @@ int femgpu_form_create(const femgpu_form_desc* d, femgpu_form** out) {
         host.insert(host.end(), f->D.begin(), f->D.end());
         host.insert(host.end(), f->P.begin(), f->P.end());
         const int npair = f->ns * (f->ns + 1) / 2;
-        const double per_q = d->kind == FEMGPU_ELASTICITY ? 24.0 : 40.0;
+        const double per_q = d->kind == FEMGPU_ELASTICITY ? 24.0 : 33.0;  // SVK: symmetric/antisymmetric split
         f->flops_per_cell = 60 + f->nq * (f->ns * 3 * 5 + 16 + npair * per_q * 2);
         f->kernel_name = d->kind == FEMGPU_ELASTICITY ? "pair_kernel<elasticity>" : "pair_kernel<svk>";
         break;

@@ -217,20 +217,26 @@ __device__ __forceinline__ void pair_point(double (&a4)[2][2][3][3], double (&t1
     for (int y = 0; y < 2; ++y)
 #pragma unroll
       for (int bb = 0; bb < 3; ++bb) hk[y][bb] = rq[(k0 + y) * JS + (3 + bb) * CELLS];
-    // qs holds mu' F F^T (pre-scaled in the setup), so g_j enters unscaled
+    // Symmetric / antisymmetric split of each 3x3 (c,d) block (svk_unfold):
+    //   lam h_j[c] h_k[d] + mu h_k[c] h_j[d] = al (h_j[c] h_k[d] + h_j[d] h_k[c])
+    //                                        + be (h_j[c] h_k[d] - h_j[d] h_k[c]),
+    // al = (lam'+mu')/2, be = (lam'-mu')/2; the mu' F F^T (g_j.g_k) term is symmetric.
+    // a4[c][d] (c<=d) holds the symmetric part (diagonal halved), a4[d][c] (c<d) the
+    // antisymmetric one: 27 instead of 33 FP64 instructions per (j,k) pair and point.
+    // qs holds al, be, then mu' F F^T with its diagonal halved (setup).
     const double f00 = qs[2 * CELLS], f01 = qs[3 * CELLS], f02 = qs[4 * CELLS];
     const double f11 = qs[5 * CELLS], f12 = qs[6 * CELLS], f22 = qs[7 * CELLS];
     const double ff[3][3] = {{f00, f01, f02}, {f01, f11, f12}, {f02, f12, f22}};
 #pragma unroll
     for (int x = 0; x < 2; ++x) {
-      double gj[3], lh[3], mh[3], s[3];
+      double gj[3], ah[3], bh[3], s[3];
       const double* r = rq + (j0 + x) * JS;
 #pragma unroll
       for (int bb = 0; bb < 3; ++bb) {
         gj[bb] = r[bb * CELLS];                // g_j
         const double h = r[(3 + bb) * CELLS];
-        lh[bb] = lq * h;                       // lam' h_j
-        mh[bb] = mq * h;                       // mu' h_j
+        ah[bb] = lq * h;                       // al h_j
+        bh[bb] = mq * h;                       // be h_j
         s[bb] = r[(6 + bb) * CELLS];           // w' S g_j
       }
       double t2[2];
@@ -240,26 +246,57 @@ __device__ __forceinline__ void pair_point(double (&a4)[2][2][3][3], double (&t1
         t1[x][y] = fma(s[0], gk[y][0], fma(s[1], gk[y][1], fma(s[2], gk[y][2], t1[x][y])));
         t2[y] = gj[0] * gk[y][0] + gj[1] * gk[y][1] + gj[2] * gk[y][2];
       }
+      // first terms: symmetric diagonal and off-diagonal, antisymmetric
 #pragma unroll
       for (int y = 0; y < 2; ++y)
 #pragma unroll
         for (int c = 0; c < 3; ++c)
 #pragma unroll
-          for (int d = 0; d < 3; ++d) a4[x][y][c][d] = fma(lh[c], hk[y][d], a4[x][y][c][d]);
+          for (int d = c; d < 3; ++d) {
+            a4[x][y][c][d] = fma(ah[c], hk[y][d], a4[x][y][c][d]);
+            if (d > c) a4[x][y][d][c] = fma(bh[c], hk[y][d], a4[x][y][d][c]);
+          }
+      // second terms of the off-diagonal entries; F F^T term of the diagonal
 #pragma unroll
       for (int y = 0; y < 2; ++y)
 #pragma unroll
         for (int c = 0; c < 3; ++c)
 #pragma unroll
-          for (int d = 0; d < 3; ++d) a4[x][y][c][d] = fma(hk[y][c], mh[d], a4[x][y][c][d]);
+          for (int d = c; d < 3; ++d) {
+            if (d > c) {
+              a4[x][y][c][d] = fma(ah[d], hk[y][c], a4[x][y][c][d]);
+              a4[x][y][d][c] = fma(-bh[d], hk[y][c], a4[x][y][d][c]);
+            } else {
+              a4[x][y][c][c] = fma(t2[y], ff[c][c], a4[x][y][c][c]);
+            }
+          }
 #pragma unroll
       for (int y = 0; y < 2; ++y)
 #pragma unroll
         for (int c = 0; c < 3; ++c)
 #pragma unroll
-          for (int d = 0; d < 3; ++d) a4[x][y][c][d] = fma(t2[y], ff[c][d], a4[x][y][c][d]);
+          for (int d = c + 1; d < 3; ++d) a4[x][y][c][d] = fma(t2[y], ff[c][d], a4[x][y][c][d]);
     }
   }
+}
+
+// SVK: symmetric (upper, diagonal halved) / antisymmetric (lower) parts -> the block.
+__device__ __forceinline__ void svk_unfold(double (&a4)[2][2][3][3]) {
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int y = 0; y < 2; ++y) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        a4[x][y][c][c] *= 2.0;
+#pragma unroll
+        for (int d = c + 1; d < 3; ++d) {
+          const double s = a4[x][y][c][d], n = a4[x][y][d][c];
+          a4[x][y][c][d] = s + n;
+          a4[x][y][d][c] = s - n;
+        }
+      }
+    }
 }
 
 // The q-summed scalar term (SVK s_j.g_k, elasticity mu' g_j.g_k) enters the
@@ -585,8 +622,13 @@ __global__ void __launch_bounds__(128, 2)
 #pragma unroll
         for (int i = 0; i < 9; ++i) Kr[i] = K[i];
         double* qs = sQs + ql * Sh::QSD * CELLS + c;
-        qs[0 * CELLS] = lamq * wq;
-        qs[1 * CELLS] = muq * wq;
+        if constexpr (Sh::SVK) {  // al, be of the symmetric / antisymmetric split
+          qs[0 * CELLS] = 0.5 * (lamq + muq) * wq;
+          qs[1 * CELLS] = 0.5 * (lamq - muq) * wq;
+        } else {
+          qs[0 * CELLS] = lamq * wq;
+          qs[1 * CELLS] = muq * wq;
+        }
         if constexpr (!Sh::SVK) {
 #pragma unroll 2
           for (int j = 0; j < NS; ++j) {
@@ -629,13 +671,14 @@ __global__ void __launch_bounds__(128, 2)
           for (int b = 0; b < 3; ++b)
             Sw[a][b] = wq * ((a == b ? lamq * trE : 0.0) + 2.0 * muq * Ee[a][b]);
         // F F^T: (0,0),(0,1),(0,2),(1,1),(1,2),(2,2)
-        const double mw = muq * wq;  // mu' F F^T: pre-scaled for the accumulate phase
-        qs[2 * CELLS] = mw * (F[0][0] * F[0][0] + F[0][1] * F[0][1] + F[0][2] * F[0][2]);
+        // mu' F F^T, pre-scaled for the accumulate phase; diagonal halved (svk_unfold)
+        const double mw = muq * wq, mh = 0.5 * mw;
+        qs[2 * CELLS] = mh * (F[0][0] * F[0][0] + F[0][1] * F[0][1] + F[0][2] * F[0][2]);
         qs[3 * CELLS] = mw * (F[0][0] * F[1][0] + F[0][1] * F[1][1] + F[0][2] * F[1][2]);
         qs[4 * CELLS] = mw * (F[0][0] * F[2][0] + F[0][1] * F[2][1] + F[0][2] * F[2][2]);
-        qs[5 * CELLS] = mw * (F[1][0] * F[1][0] + F[1][1] * F[1][1] + F[1][2] * F[1][2]);
+        qs[5 * CELLS] = mh * (F[1][0] * F[1][0] + F[1][1] * F[1][1] + F[1][2] * F[1][2]);
         qs[6 * CELLS] = mw * (F[1][0] * F[2][0] + F[1][1] * F[2][1] + F[1][2] * F[2][2]);
-        qs[7 * CELLS] = mw * (F[2][0] * F[2][0] + F[2][1] * F[2][1] + F[2][2] * F[2][2]);
+        qs[7 * CELLS] = mh * (F[2][0] * F[2][0] + F[2][1] * F[2][1] + F[2][2] * F[2][2]);
 #pragma unroll 2
         for (int j = 0; j < NS; ++j) {
           double g[3];
@@ -664,6 +707,7 @@ __global__ void __launch_bounds__(128, 2)
       }
       __syncthreads();  // records consumed (next chunk / staging overwrite them)
     }
+    if constexpr (Sh::SVK) svk_unfold(a4);
     add_t1(a4, t1);
     if (sl.active) pair_stage<Sh>(sU + sl.cell * Sh::CSTRIDE, a4, sl);
     fence_proxy_async();
