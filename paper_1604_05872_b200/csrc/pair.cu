@@ -28,15 +28,20 @@
 //    conflict-free 16-byte stores) and written by TMA bulk copies
 //    (cp.async.bulk, or cp.reduce.async.bulk .add.f64 for the += contract).
 //
-// Two CTA organisations (chosen per form by measurement, profiles/):
+// CTA organisations (chosen per form by measurement, profiles/):
 //  * pair_ws_kernel  (elasticity): warp-specialised -- 2 producer warps build
 //    the records of the next tile into a double buffer (mbarrier full/empty)
 //    while 4 consumer warps accumulate; 2 CTAs per SM;
-//  * pair_flat_kernel (SVK): every thread takes part in each phase (per-point
-//    tensors, records, accumulation); 2 CTAs per SM overlap one CTA's
-//    latency-bound setup with the other's FMA stream.  (A producer/consumer
-//    split was measured slower here: the per-point F, E, S work is ~20% of
-//    the FLOPs and too latency-bound for a minority of warps.)
+//  * pair_svk_ws_kernel (SVK): warp-specialised with a deeper ring -- 4 producer
+//    warps run the heavier per-point setup (F, E, S, F F^T, 10 records per (cell, q))
+//    into a 5-slot ring of 2-point stages while 8 consumer warps (2 cells each)
+//    accumulate; one CTA of 16 cells per SM pools the shared memory for the ring;
+//  * pair_flat_kernel (SVK before, PAIR_SVK_WS=0): every thread takes part in each
+//    phase; 2 CTAs per SM overlap one CTA's setup with the other's FMA stream
+//    (c4 1.31 ms against 1.25 ms for the ring kernel).
+//
+// SVK accumulates each 3x3 (c,d) block as its symmetric and antisymmetric parts
+// (pair_point, svk_unfold): 27 instead of 33 FP64 instructions per pair and point.
 #include "common.cuh"
 #include "femgpu_internal.h"
 #include "../../include/femgpu.h"
@@ -53,8 +58,27 @@
 #ifndef PAIR_ELAS_FLAT
 #define PAIR_ELAS_FLAT 0
 #endif
+#ifndef PAIR_FLAT_CTAS
+#define PAIR_FLAT_CTAS 2  // CTAs per SM of the flat (SVK) kernel
+#endif
+#ifndef PAIR_SVK_QC
+#define PAIR_SVK_QC 14  // SVK quadrature points per chunk (14 -> 112 of 128 threads busy in the setup)
+#endif
+#ifndef PAIR_SVK_WS
+#define PAIR_SVK_WS 1  // SVK: warp-specialised kernel (1) or the flat one (0)
+#endif
+#ifndef PAIR_SVK_CELLS
+#define PAIR_SVK_CELLS 16  // SVK ws: cells per CTA tile (8: 2 CTAs per SM, 16: one)
+#endif
+#ifndef PAIR_SVK_SLOTS
+#define PAIR_SVK_SLOTS 5  // SVK ws: record ring slots (0: one per producer warp)
+#endif
+#ifndef PAIR_SVK_PW
+#define PAIR_SVK_PW 4  // SVK ws: producer warps
+#endif
 #ifndef PAIR_ABL  // development ablations of pair_ws_kernel: bit 0 no accumulate, bit 1 no store,
                   // bit 2 no records, bit 3 no geometry, bit 4 no staging
+                  // (pair_flat_kernel: bit 0 no accumulate, bit 2 no per-point setup)
 #define PAIR_ABL 0
 #endif
 
@@ -74,9 +98,9 @@ struct PairShape {
   static constexpr bool FLAT = SVK || PAIR_ELAS_FLAT;    // organisation (see header)
   static constexpr int PROD = FLAT ? 0 : 64;             // producer threads (ws kernel only)
   static constexpr int THREADS = ACC + PROD;
-  static constexpr int CTAS_PER_SM = 2;
+  static constexpr int CTAS_PER_SM = FLAT ? PAIR_FLAT_CTAS : 2;
   static constexpr int NCOEF = SVK ? 3 * NS + 8 : 8;
-  static constexpr int QC = SVK ? 14 : Q;                // quadrature points per chunk (SVK: 14 -> 112 of 128 threads busy in the setup phase)
+  static constexpr int QC = SVK ? PAIR_SVK_QC : Q;       // quadrature points per chunk
   static constexpr int NCHUNK = (Q + QC - 1) / QC;
   static constexpr int RECD = SVK ? 9 : 3;               // per (q,j): g | h | s
   static constexpr int QSD = SVK ? 8 : 2;                // per q: lam', mu' | F F^T (6)
@@ -297,6 +321,100 @@ __device__ __forceinline__ void svk_unfold(double (&a4)[2][2][3][3]) {
         }
       }
     }
+}
+
+// Per (cell, quadrature point) setup, one thread: lam', mu' (and, SVK: F = I + grad w,
+// E, w'S, mu' F F^T), then the records of the NS basis functions at q: g_j = K^T D phi_j
+// (elasticity), plus h_j = F g_j and s_j = w' S g_j (SVK).  qs / rec: this cell's
+// per-point scalars (stride CELLS) and records (j stride JS, component stride CELLS).
+template <bool SVK, int NS, int Q, int CELLS, int JS, int NCOEF>
+__device__ __forceinline__ void pair_point_setup(const double* K, const double* cf, bool valid,
+                                                 int q, const double* sW, const double* sD,
+                                                 const double* sP, double* qs, double* rec) {
+  auto cv = [&](int r) -> double { return valid ? cf[r] : 0.0; };
+  constexpr int CO = SVK ? 3 * NS : 0;  // offset of mu, lam in the dofs
+  double muq = 0, lamq = 0;
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    muq += cv(CO + m) * sP[q * 4 + m];
+    lamq += cv(CO + 4 + m) * sP[q * 4 + m];
+  }
+  const double wq = sW[q] * K[9];
+  double Kr[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) Kr[i] = K[i];
+  if constexpr (!SVK) {
+    qs[0 * CELLS] = lamq * wq;
+    qs[1 * CELLS] = muq * wq;
+#pragma unroll 2
+    for (int j = 0; j < NS; ++j) {
+      double* rr = rec + j * JS;
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+        rr[b * CELLS] = Kr[0 * 3 + b] * sD[(0 * Q + q) * NS + j] +
+                        Kr[1 * 3 + b] * sD[(1 * Q + q) * NS + j] +
+                        Kr[2 * 3 + b] * sD[(2 * Q + q) * NS + j];
+    }
+  } else {
+    // al, be of the symmetric / antisymmetric split (pair_point, svk_unfold)
+    qs[0 * CELLS] = 0.5 * (lamq + muq) * wq;
+    qs[1 * CELLS] = 0.5 * (lamq - muq) * wq;
+    double F[3][3];
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc) {
+      double gr[3] = {0, 0, 0};  // reference gradient of w_cc
+#pragma unroll
+      for (int m = 0; m < NS; ++m) {
+        const double wm = cv(cc * NS + m);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) gr[a] += wm * sD[(a * Q + q) * NS + m];
+      }
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+        F[cc][b] = (cc == b ? 1.0 : 0.0) + gr[0] * Kr[0 * 3 + b] + gr[1] * Kr[1 * 3 + b] +
+                   gr[2] * Kr[2 * 3 + b];
+    }
+    double Ee[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        const double t = F[0][a] * F[0][b] + F[1][a] * F[1][b] + F[2][a] * F[2][b];
+        Ee[a][b] = 0.5 * (a == b ? t - 1.0 : t);
+      }
+    const double trE = Ee[0][0] + Ee[1][1] + Ee[2][2];
+    double Sw[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+        Sw[a][b] = wq * ((a == b ? lamq * trE : 0.0) + 2.0 * muq * Ee[a][b]);
+    // mu' F F^T (0,0),(0,1),(0,2),(1,1),(1,2),(2,2), pre-scaled for the accumulate
+    // phase; diagonal halved (svk_unfold)
+    const double mw = muq * wq, mh = 0.5 * mw;
+    qs[2 * CELLS] = mh * (F[0][0] * F[0][0] + F[0][1] * F[0][1] + F[0][2] * F[0][2]);
+    qs[3 * CELLS] = mw * (F[0][0] * F[1][0] + F[0][1] * F[1][1] + F[0][2] * F[1][2]);
+    qs[4 * CELLS] = mw * (F[0][0] * F[2][0] + F[0][1] * F[2][1] + F[0][2] * F[2][2]);
+    qs[5 * CELLS] = mh * (F[1][0] * F[1][0] + F[1][1] * F[1][1] + F[1][2] * F[1][2]);
+    qs[6 * CELLS] = mw * (F[1][0] * F[2][0] + F[1][1] * F[2][1] + F[1][2] * F[2][2]);
+    qs[7 * CELLS] = mh * (F[2][0] * F[2][0] + F[2][1] * F[2][1] + F[2][2] * F[2][2]);
+#pragma unroll 2
+    for (int j = 0; j < NS; ++j) {
+      double g[3];
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+        g[b] = Kr[0 * 3 + b] * sD[(0 * Q + q) * NS + j] + Kr[1 * 3 + b] * sD[(1 * Q + q) * NS + j] +
+               Kr[2 * 3 + b] * sD[(2 * Q + q) * NS + j];
+      double* rr = rec + j * JS;
+#pragma unroll
+      for (int b = 0; b < 3; ++b) rr[b * CELLS] = g[b];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        rr[(3 + a) * CELLS] = F[a][0] * g[0] + F[a][1] * g[1] + F[a][2] * g[2];
+        rr[(6 + a) * CELLS] = Sw[a][0] * g[0] + Sw[a][1] * g[1] + Sw[a][2] * g[2];
+      }
+    }
+  }
 }
 
 // The q-summed scalar term (SVK s_j.g_k, elasticity mu' g_j.g_k) enters the
@@ -540,7 +658,7 @@ __global__ void __launch_bounds__(PairShape<FEMGPU_ELASTICITY, NS, Q>::THREADS, 
 // St Venant-Kirchhoff: flat (all threads in every phase), 2 CTAs per SM
 // ============================================================================
 template <int KIND, int NS, int Q>
-__global__ void __launch_bounds__(128, 2)
+__global__ void __launch_bounds__(128, PAIR_FLAT_CTAS)
     pair_flat_kernel(long E, const double* __restrict__ coords, const double* __restrict__ coef,
                      const double* __restrict__ tab, double* __restrict__ A, int acc) {
   using Sh = PairShape<KIND, NS, Q>;
@@ -589,9 +707,6 @@ __global__ void __launch_bounds__(128, 2)
       cd[9] = g.adet;
     }
     __syncthreads();
-    auto coefv = [&](int c, int r) -> double {
-      return c < nt ? sIn[CELLS * 12 + c * Sh::NCOEF + r] : 0.0;
-    };
     double a4[2][2][3][3];
     double t1[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // SVK: sum_q s_j.g_k; elasticity: mu' g_j.g_k
     zero_tile(a4);
@@ -604,102 +719,18 @@ __global__ void __launch_bounds__(128, 2)
       // warp-owned cells (JS odd): q and q + 4 share a half-warp, so the record
       // stores of its 16 lanes fall in opposite bank halves
       constexpr int NTASK = Sh::WARP_CELLS ? CELLS * ((Sh::QC + 7) / 8 * 8) : CELLS * Sh::QC;
-      for (int task = tid; task < NTASK; task += Sh::THREADS) {
+      for (int task = tid; task < ((PAIR_ABL & 4) ? 0 : NTASK); task += Sh::THREADS) {
         const int c = task % CELLS, r = task / CELLS;
         const int ql = Sh::WARP_CELLS ? (r >> 3) * 8 + (r & 1) * 4 + ((r & 7) >> 1) : r;
         if (ql >= qn) continue;
         const int q = q0 + ql;
-        const double* K = sCell + c * Sh::CELLD;
-        constexpr int CO = Sh::SVK ? 3 * NS : 0;  // offset of mu, lam in the dofs
-        double muq = 0, lamq = 0;
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          muq += coefv(c, CO + m) * sP[q * 4 + m];
-          lamq += coefv(c, CO + 4 + m) * sP[q * 4 + m];
-        }
-        const double wq = sW[q] * K[9];
-        double Kr[9];
-#pragma unroll
-        for (int i = 0; i < 9; ++i) Kr[i] = K[i];
-        double* qs = sQs + ql * Sh::QSD * CELLS + c;
-        if constexpr (Sh::SVK) {  // al, be of the symmetric / antisymmetric split
-          qs[0 * CELLS] = 0.5 * (lamq + muq) * wq;
-          qs[1 * CELLS] = 0.5 * (lamq - muq) * wq;
-        } else {
-          qs[0 * CELLS] = lamq * wq;
-          qs[1 * CELLS] = muq * wq;
-        }
-        if constexpr (!Sh::SVK) {
-#pragma unroll 2
-          for (int j = 0; j < NS; ++j) {
-            double* rr = sU + (ql * NS + j) * Sh::JS + c;
-#pragma unroll
-            for (int b = 0; b < 3; ++b)
-              rr[b * CELLS] = Kr[0 * 3 + b] * sD[(0 * Q + q) * NS + j] +
-                              Kr[1 * 3 + b] * sD[(1 * Q + q) * NS + j] +
-                              Kr[2 * 3 + b] * sD[(2 * Q + q) * NS + j];
-          }
-        } else {
-        double F[3][3];
-#pragma unroll
-        for (int cc = 0; cc < 3; ++cc) {
-          double gr[3] = {0, 0, 0};  // reference gradient of w_cc
-#pragma unroll
-          for (int m = 0; m < NS; ++m) {
-            const double wm = coefv(c, cc * NS + m);
-#pragma unroll
-            for (int a = 0; a < 3; ++a) gr[a] += wm * sD[(a * Q + q) * NS + m];
-          }
-#pragma unroll
-          for (int b = 0; b < 3; ++b)
-            F[cc][b] = (cc == b ? 1.0 : 0.0) + gr[0] * Kr[0 * 3 + b] + gr[1] * Kr[1 * 3 + b] +
-                       gr[2] * Kr[2 * 3 + b];
-        }
-        double Ee[3][3];
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-#pragma unroll
-          for (int b = 0; b < 3; ++b) {
-            const double t = F[0][a] * F[0][b] + F[1][a] * F[1][b] + F[2][a] * F[2][b];
-            Ee[a][b] = 0.5 * (a == b ? t - 1.0 : t);
-          }
-        const double trE = Ee[0][0] + Ee[1][1] + Ee[2][2];
-        double Sw[3][3];
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-#pragma unroll
-          for (int b = 0; b < 3; ++b)
-            Sw[a][b] = wq * ((a == b ? lamq * trE : 0.0) + 2.0 * muq * Ee[a][b]);
-        // F F^T: (0,0),(0,1),(0,2),(1,1),(1,2),(2,2)
-        // mu' F F^T, pre-scaled for the accumulate phase; diagonal halved (svk_unfold)
-        const double mw = muq * wq, mh = 0.5 * mw;
-        qs[2 * CELLS] = mh * (F[0][0] * F[0][0] + F[0][1] * F[0][1] + F[0][2] * F[0][2]);
-        qs[3 * CELLS] = mw * (F[0][0] * F[1][0] + F[0][1] * F[1][1] + F[0][2] * F[1][2]);
-        qs[4 * CELLS] = mw * (F[0][0] * F[2][0] + F[0][1] * F[2][1] + F[0][2] * F[2][2]);
-        qs[5 * CELLS] = mh * (F[1][0] * F[1][0] + F[1][1] * F[1][1] + F[1][2] * F[1][2]);
-        qs[6 * CELLS] = mw * (F[1][0] * F[2][0] + F[1][1] * F[2][1] + F[1][2] * F[2][2]);
-        qs[7 * CELLS] = mh * (F[2][0] * F[2][0] + F[2][1] * F[2][1] + F[2][2] * F[2][2]);
-#pragma unroll 2
-        for (int j = 0; j < NS; ++j) {
-          double g[3];
-#pragma unroll
-          for (int b = 0; b < 3; ++b)
-            g[b] = Kr[0 * 3 + b] * sD[(0 * Q + q) * NS + j] + Kr[1 * 3 + b] * sD[(1 * Q + q) * NS + j] +
-                   Kr[2 * 3 + b] * sD[(2 * Q + q) * NS + j];
-          double* rr = sU + (ql * NS + j) * Sh::JS + c;
-#pragma unroll
-          for (int b = 0; b < 3; ++b) rr[b * CELLS] = g[b];
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            rr[(3 + a) * CELLS] = F[a][0] * g[0] + F[a][1] * g[1] + F[a][2] * g[2];
-            rr[(6 + a) * CELLS] = Sw[a][0] * g[0] + Sw[a][1] * g[1] + Sw[a][2] * g[2];
-          }
-        }
-        }
+        pair_point_setup<Sh::SVK, NS, Q, CELLS, Sh::JS, Sh::NCOEF>(
+            sCell + c * Sh::CELLD, sIn + CELLS * 12 + c * Sh::NCOEF, c < nt, q, sW, sD, sP,
+            sQs + ql * Sh::QSD * CELLS + c, sU + ql * NS * Sh::JS + c);
       }
       __syncthreads();
       if (ch == Sh::NCHUNK - 1 && tile + gridDim.x < ntiles) prefetch(tile + gridDim.x);
-      if (sl.active) {
+      if (sl.active && !(PAIR_ABL & 1)) {
 #pragma unroll kPairQUnroll
         for (int ql = 0; ql < qn; ++ql)
           pair_point<Sh>(a4, t1, sU + ql * NS * Sh::JS + sl.cell,
@@ -717,10 +748,218 @@ __global__ void __launch_bounds__(128, 2)
   if (tid == 0) bulk_wait0();
 }
 
+
+// ============================================================================
+// St Venant-Kirchhoff, warp-specialised: NPW producer warps run the per-point setup
+// (one (cell, q) per lane: 32 / CELLS points x CELLS cells per ring stage) into an
+// NPW-slot record ring -- producer warp p fills slot p, so each has NPW - 1 stages
+// of lead -- while the consumer warps accumulate; each consumer warp owns 2 cells
+// (15 (j,k) tiles each) and stages / bulk-stores them one at a time through its own
+// 7.2 KB buffer.  CELLS = 8: 2 CTAs x (4 + NPW) warps per SM; CELLS = 16: one CTA
+// of 8 + NPW warps pooling the shared memory into a deeper ring.
+// ============================================================================
+template <int NS_, int Q>
+struct SvkWsShape {
+  static constexpr bool SVK = true;
+  static constexpr int NS = NS_;
+  static constexpr int N = 3 * NS;
+  static constexpr int NJ = NS / 2;
+  static constexpr int NTILE = NJ * (NJ + 1) / 2;
+  static constexpr int CELLS = PAIR_SVK_CELLS;
+  static constexpr int NPW = PAIR_SVK_PW;               // producer warps (stage g: warp g % NPW)
+  static constexpr int NSLOT = PAIR_SVK_SLOTS > 0 ? PAIR_SVK_SLOTS : NPW;  // ring slots
+  static constexpr int WCELLS = 2;                      // cells per consumer warp
+  static constexpr int ACC = 32 * CELLS / WCELLS, PROD = 32 * NPW, THREADS = ACC + PROD;
+  static constexpr int CTAS_PER_SM = CELLS == 8 ? 2 : 1;
+  static constexpr bool WARP_CELLS = true;
+  static constexpr int QS = 32 / CELLS;                 // points per ring stage
+  static constexpr int NST = (Q + QS - 1) / QS;         // ring stages per tile
+  static constexpr int RECD = 9, QSD = 8;
+  static constexpr int JS = RECD * CELLS + 1;           // odd: conflict-free warp-cell loads
+  static constexpr int STAGE_DBL = QS * (NS * JS + QSD * CELLS);
+  static constexpr int NCOEF = 3 * NS + 8;
+  static constexpr int TAB0 = Q + 3 * Q * NS + 4 * Q;
+  static constexpr int TAB = (TAB0 + 1) / 2 * 2;
+  static constexpr int CELLD = 10;
+  static constexpr int IN_DBL = CELLS * (12 + NCOEF);
+  static constexpr int CSTRIDE = N * N;                  // one cell per staging buffer
+  static constexpr int HEAD = TAB + 2 * (CELLS * CELLD + IN_DBL);  // double-buffered per tile
+  static constexpr size_t SMEM = sizeof(double) * ((size_t)HEAD + NSLOT * STAGE_DBL +
+                                                   (ACC / 32) * CSTRIDE) +
+                                 2 * NSLOT * sizeof(uint64_t);
+  static_assert(WCELLS * NTILE <= 32 && QS * CELLS == 32, "lane maps");
+  static_assert(HEAD % 2 == 0 && STAGE_DBL % 2 == 0 && CSTRIDE % 2 == 0, "16-byte aligned buffers");
+};
+
+template <int NS, int Q>
+__global__ void __launch_bounds__(SvkWsShape<NS, Q>::THREADS, SvkWsShape<NS, Q>::CTAS_PER_SM)
+    pair_svk_ws_kernel(long E, const double* __restrict__ coords, const double* __restrict__ coef,
+                       const double* __restrict__ tab, double* __restrict__ A, int acc) {
+  using Sh = SvkWsShape<NS, Q>;
+  constexpr int CELLS = Sh::CELLS, NPW = Sh::NPW, NSLOT = Sh::NSLOT;
+  extern __shared__ __align__(16) double smem[];
+  double* sW = smem;
+  double* sD = sW + Q;                        // [3][Q][NS]
+  double* sP = sD + 3 * Q * NS;               // [Q][4]
+  double* sCell = smem + Sh::TAB;             // [2][CELLS][CELLD]          (producers)
+  double* sIn = sCell + 2 * CELLS * Sh::CELLD;  // [2][CELLS][12 | NCOEF]   (producers)
+  double* sRing = smem + Sh::HEAD;            // [NSLOT][STAGE_DBL]  producers -> consumers
+  double* sStg = sRing + NSLOT * Sh::STAGE_DBL;  // [consumer warps][CSTRIDE]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStg + (Sh::ACC / 32) * Sh::CSTRIDE);
+  uint64_t* empty = full + NSLOT;
+  // stage: rec[(ql*NS + j)*JS + comp*CELLS + cell], then qs[(ql*QSD + x)*CELLS + cell]
+
+  const int tid = threadIdx.x;
+  const long ntiles = (E + CELLS - 1) / CELLS;
+  if ((long)blockIdx.x >= ntiles) return;
+  const long my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+
+  for (int i = tid; i < Sh::TAB0; i += Sh::THREADS) smem[i] = tab[i];
+  if (tid == 0) {
+    for (int b = 0; b < NSLOT; ++b) {
+      mbar_init(&full[b], 32);
+      mbar_init(&empty[b], Sh::ACC / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (tid < Sh::ACC) {
+    // ---------------- consumers ----------------
+    const PairSlot sl = pair_slot<Sh>(tid);
+    const int lane = tid & 31, warp = tid >> 5;
+    double* stg = sStg + warp * Sh::CSTRIDE;
+    long g = 0;  // ring stage counter: slot g % NSLOT, use g / NSLOT
+    for (long it = 0; it < my_tiles; ++it) {
+      const long c0 = (blockIdx.x + it * gridDim.x) * CELLS;
+      const int nt = (int)min((long)CELLS, E - c0);
+      double a4[2][2][3][3];
+      double t1[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // sum_q s_j.g_k
+      zero_tile(a4);
+#pragma unroll 1
+      for (int st = 0; st < Sh::NST; ++st, ++g) {
+        const int b = (int)(g % NSLOT);
+        mbar_wait(&full[b], (uint32_t)((g / NSLOT) & 1));
+        const double* rec = sRing + b * Sh::STAGE_DBL;
+        const double* qsb = rec + Sh::QS * NS * Sh::JS;
+        if (sl.active && !(PAIR_ABL & 1)) {
+          if (st * Sh::QS + Sh::QS <= Q) {
+#pragma unroll
+            for (int ql = 0; ql < Sh::QS; ++ql)
+              pair_point<Sh>(a4, t1, rec + ql * NS * Sh::JS + sl.cell,
+                             qsb + ql * Sh::QSD * CELLS + sl.cell, sl.j0, sl.k0);
+          } else {
+            for (int ql = 0; ql < Q - st * Sh::QS; ++ql)
+              pair_point<Sh>(a4, t1, rec + ql * NS * Sh::JS + sl.cell,
+                             qsb + ql * Sh::QSD * CELLS + sl.cell, sl.j0, sl.k0);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cta(&empty[b]);
+      }
+      svk_unfold(a4);
+      add_t1(a4, t1);
+      // this warp's cells, one at a time through its staging buffer
+#pragma unroll 1
+      for (int cc = 0; cc < Sh::WCELLS; ++cc) {
+        const int cell = warp * Sh::WCELLS + cc;
+        if (lane == 0) bulk_wait_read0();  // the previous bulk store has read the buffer
+        __syncwarp();
+        if (sl.active && sl.cell == cell) pair_stage<Sh>(stg, a4, sl);
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0 && cell < nt) {
+          double* dst = A + (c0 + cell) * (size_t)Sh::N * Sh::N;
+          if (acc)
+            bulk_s2g_add(dst, stg, Sh::N * Sh::N * 8);
+          else
+            bulk_s2g(dst, stg, Sh::N * Sh::N * 8);
+          bulk_commit();
+        }
+      }
+    }
+    if (lane == 0) bulk_wait0();
+  } else {
+    // ---------------- producer warps: inputs (cp.async, one tile ahead), geometry,
+    //                  per-point setup; warp pw takes stages g = pw mod NPW ----------------
+    const int ptid = tid - Sh::ACC, pt = ptid & 31, pw = ptid >> 5;
+    auto prefetch = [&](long it) {
+      const long c0 = (blockIdx.x + it * gridDim.x) * CELLS;
+      const int nt = (int)min((long)CELLS, E - c0);
+      double* in = sIn + (it & 1) * Sh::IN_DBL;
+      for (int i = ptid; i < nt * 12; i += Sh::PROD) cp_async8(&in[i], coords + c0 * 12 + i);
+      for (int i = ptid; i < nt * Sh::NCOEF; i += Sh::PROD)
+        cp_async8(&in[CELLS * 12 + i], coef + c0 * Sh::NCOEF + i);
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    prefetch(0);
+    const int c = pt % CELLS, ql = pt / CELLS;
+    long g = 0;
+    for (long it = 0; it < my_tiles; ++it) {
+      const long c0 = (blockIdx.x + it * gridDim.x) * CELLS;
+      const int nt = (int)min((long)CELLS, E - c0);
+      const double* in = sIn + (it & 1) * Sh::IN_DBL;
+      double* cell = sCell + (it & 1) * CELLS * Sh::CELLD;
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      named_bar(1, Sh::PROD);  // this tile's inputs have landed (all producer threads' copies)
+      if (ptid < CELLS) {
+        double x[12];
+#pragma unroll
+        for (int r = 0; r < 12; ++r)  // cells past the end: reference tet (never stored)
+          x[r] = ptid < nt ? in[ptid * 12 + r] : ((r == 3 || r == 7 || r == 11) ? 1.0 : 0.0);
+        const Geo geo = cell_geometry(x);
+        double* cd = cell + ptid * Sh::CELLD;
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int bb = 0; bb < 3; ++bb) cd[a * 3 + bb] = geo.K[a][bb];
+        cd[9] = geo.adet;
+      }
+      // geometry visible; every producer is past the previous tile, whose input buffer
+      // the next prefetch overwrites
+      named_bar(1, Sh::PROD);
+      if (it + 1 < my_tiles) prefetch(it + 1);
+#pragma unroll 1
+      for (int st = 0; st < Sh::NST; ++st, ++g) {
+        if ((int)(g % NPW) != pw) continue;
+        const int b = (int)(g % NSLOT);
+        if (g >= NSLOT) mbar_wait(&empty[b], (uint32_t)((g / NSLOT - 1) & 1));
+        double* rec = sRing + b * Sh::STAGE_DBL;
+        const int q = st * Sh::QS + ql;
+        if (q < Q && !(PAIR_ABL & 4))
+          pair_point_setup<true, NS, Q, CELLS, Sh::JS, Sh::NCOEF>(
+              cell + c * Sh::CELLD, in + CELLS * 12 + c * Sh::NCOEF, c < nt, q, sW, sD, sP,
+              rec + Sh::QS * NS * Sh::JS + ql * Sh::QSD * CELLS + c, rec + ql * NS * Sh::JS + c);
+        mbar_arrive_cta(&full[b]);  // release: this stage's records are visible
+      }
+    }
+  }
+}
+
+template <int NS, int Q>
+static cudaError_t launch_svk_ws(long E, const double* coords, const double* coef,
+                                 const double* tab, double* A, int acc, cudaStream_t s) {
+  using Sh = SvkWsShape<NS, Q>;
+  auto kern = pair_svk_ws_kernel<NS, Q>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::SMEM);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const long ntiles = (E + Sh::CELLS - 1) / Sh::CELLS;
+  const long maxc = (long)Sh::CTAS_PER_SM * kNumSMs;
+  const int grid = (int)(ntiles < maxc ? ntiles : maxc);
+  kern<<<grid, Sh::THREADS, Sh::SMEM, s>>>(E, coords, coef, tab, A, acc);
+  return cudaGetLastError();
+}
+
 template <int KIND, int NS, int Q>
 static cudaError_t launch_pair_t(long E, const double* coords, const double* coef,
                                  const double* tab, double* A, int acc, cudaStream_t s) {
   using Sh = PairShape<KIND, NS, Q>;
+  if constexpr (Sh::SVK && PAIR_SVK_WS) return launch_svk_ws<NS, Q>(E, coords, coef, tab, A, acc, s);
   auto kern = (Sh::SVK || Sh::FLAT) ? pair_flat_kernel<KIND, NS, Q> : pair_ws_kernel<NS, Q>;
   static bool configured = false;
   if (!configured) {
