@@ -22,6 +22,7 @@
 #define FEMGPU_H
 
 #include <stddef.h>
+#include <stdint.h>
 
 #ifdef __cplusplus
 extern "C" {
@@ -164,6 +165,22 @@ int femgpu_csr_positions(long ncells, int n, const int* dof_map, const long* row
  * A = the element matrices [ncells][n][n] of femgpu_assemble). */
 int femgpu_scatter_add(long nentries, const double* A, const long* pos, double* vals,
                        void* stream);
+
+/* Symbolic, once per mesh, for femgpu_csr_gather_rows: loc[e][j][k] =
+ * pos[e][j][k] - row_ptr[dof_map[e][j]], the entry's offset inside its CSR row
+ * (rows of at most 65536 entries).  Synchronizes the stream;
+ * FEMGPU_ERR_INCONSISTENT_LAYOUT if an entry lies outside its row. */
+int femgpu_csr_row_offsets(long ncells, int n, const int* dof_map, const long* row_ptr,
+                           const long* pos, uint16_t* loc, void* stream);
+
+/* Numeric assembly without atomics: one warp per CSR row r sums the element-matrix
+ * rows incident to it -- inc[inc_ptr[r] .. inc_ptr[r+1]) holds the element-row ids
+ * e*n + j with dof_map[e][j] == r -- in that order (bit-reproducible), then
+ * writes the row once: vals (=, or += with accumulate).  n <= 64; max_row_len =
+ * the longest CSR row. */
+int femgpu_csr_gather_rows(long nrows, int n, const long* row_ptr, const long* inc_ptr,
+                           const int* inc, const uint16_t* loc, int max_row_len,
+                           const double* A, double* vals, int accumulate, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Any femopt kernel: the GPU counterpart of femopt's

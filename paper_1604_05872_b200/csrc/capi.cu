@@ -684,6 +684,44 @@ int femgpu_scatter_add(long nentries, const double* A, const long* pos, double* 
   });
 }
 
+int femgpu_csr_row_offsets(long ncells, int n, const int* dof_map, const long* row_ptr,
+                           const long* pos, uint16_t* loc, void* stream) {
+  return guarded([&] {
+    if (ncells < 0 || n <= 0) throw Error(FEMGPU_ERR_INVALID_ARG, "bad size");
+    if (ncells == 0) return;
+    if (!dof_map || !row_ptr || !pos || !loc) throw Error(FEMGPU_ERR_INVALID_ARG, "null buffer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int* d_bad = nullptr;
+    cuda_check(cudaMallocAsync(&d_bad, sizeof(int), s), "cudaMallocAsync");
+    cuda_check(cudaMemsetAsync(d_bad, 0, sizeof(int), s), "cudaMemsetAsync");
+    cudaError_t e = femgpu::launch_csr_row_offsets(ncells, n, dof_map, row_ptr, pos, loc, d_bad, s);
+    int bad = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFreeAsync(d_bad, s);
+    cuda_check(e, "csr_row_offsets_kernel");
+    if (bad)
+      throw Error(FEMGPU_ERR_INCONSISTENT_LAYOUT,
+                  std::to_string(bad) + " element-matrix entries outside their CSR row");
+  });
+}
+
+int femgpu_csr_gather_rows(long nrows, int n, const long* row_ptr, const long* inc_ptr,
+                           const int* inc, const uint16_t* loc, int max_row_len,
+                           const double* A, double* vals, int accumulate, void* stream) {
+  return guarded([&] {
+    if (nrows < 0 || n <= 0 || n > 64) throw Error(FEMGPU_ERR_INVALID_ARG, "bad size (n <= 64)");
+    if (nrows == 0) return;
+    if (max_row_len <= 0 || max_row_len > 65536)
+      throw Error(FEMGPU_ERR_INVALID_ARG, "max_row_len out of range");
+    if (!row_ptr || !inc_ptr || !inc || !loc || !A || !vals)
+      throw Error(FEMGPU_ERR_INVALID_ARG, "null buffer");
+    cuda_check(femgpu::launch_csr_gather_rows(nrows, n, max_row_len, row_ptr, inc_ptr, inc, loc, A,
+                                              accumulate, vals, static_cast<cudaStream_t>(stream)),
+               "csr_gather_rows_kernel");
+  });
+}
+
 const char* femgpu_last_error(void) { return g_last_error.c_str(); }
 
 const char* femgpu_version(void) { return "femgpu 0.1 (sm_100a, FP64)"; }

@@ -53,6 +53,11 @@ cudaError_t launch_csr_positions(long E, int n, const int* dof, const long* row_
                                  const int* col_idx, long* pos, int* missing, cudaStream_t s);
 cudaError_t launch_scatter_add(long total, const double* A, const long* pos, double* vals,
                                cudaStream_t s);
+cudaError_t launch_csr_row_offsets(long E, int n, const int* dof, const long* row_ptr,
+                                   const long* pos, uint16_t* loc, int* bad, cudaStream_t s);
+cudaError_t launch_csr_gather_rows(long nrows, int n, int maxlen, const long* row_ptr,
+                                   const long* inc_ptr, const int* inc, const uint16_t* loc,
+                                   const double* A, int acc, double* vals, cudaStream_t s);
 
 // Burgers tensor schedule (see burgers.cu).
 bool burgers_supported(int nq, int ns);

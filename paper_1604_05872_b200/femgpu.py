@@ -41,7 +41,7 @@ ERROR_NAMES = {
 EXPORTS = ("femgpu_form_create", "femgpu_form_free", "femgpu_form_get_info", "femgpu_assemble",
            "femgpu_assemble_host", "femgpu_kernel_argv", "femgpu_kernel_argc",
            "femgpu_kernel_argname", "femgpu_gather", "femgpu_csr_positions",
-           "femgpu_scatter_add", "femgpu_assemble_csr", "femgpu_ir_create", "femgpu_ir_free", "femgpu_ir_get_info",
+           "femgpu_scatter_add", "femgpu_csr_row_offsets", "femgpu_csr_gather_rows", "femgpu_assemble_csr", "femgpu_ir_create", "femgpu_ir_free", "femgpu_ir_get_info",
            "femgpu_ir_argname", "femgpu_ir_arg_size", "femgpu_ir_source", "femgpu_ir_launch",
            "femgpu_ir_argv", "femgpu_last_error", "femgpu_version")
 
@@ -94,6 +94,9 @@ def lib():
         L.femgpu_gather.argtypes = [C.c_long, C.c_int, vp, vp, vp, vp, vp, vp, vp]
         L.femgpu_csr_positions.argtypes = [C.c_long, C.c_int, vp, vp, vp, vp, vp]
         L.femgpu_scatter_add.argtypes = [C.c_long, vp, vp, vp, vp]
+        L.femgpu_csr_row_offsets.argtypes = [C.c_long, C.c_int, vp, vp, vp, vp, vp]
+        L.femgpu_csr_gather_rows.argtypes = [C.c_long, C.c_int, vp, vp, vp, vp, C.c_int, vp, vp,
+                                             C.c_int, vp]
         L.femgpu_assemble_csr.argtypes = [vp, C.c_long, vp, vp, vp, vp, vp]
         _lib = L
     return _lib
@@ -255,3 +258,20 @@ def scatter_add(A, pos, vals, stream=None):
     """vals[pos[i]] += A[i] over all element-matrix entries."""
     _check(lib().femgpu_scatter_add(int(A.numel()), _devptr(A), _devptr(pos), _devptr(vals),
                                     _stream(stream)))
+
+
+def csr_row_offsets(dof_map, row_ptr, pos, loc, stream=None):
+    """loc[e][j][k] = pos[e][j][k] - row_ptr[dof_map[e][j]] as uint16 (synchronizes)."""
+    E, n = int(dof_map.shape[0]), int(dof_map.shape[1])
+    _check(lib().femgpu_csr_row_offsets(E, n, _devptr(dof_map), _devptr(row_ptr), _devptr(pos),
+                                        _devptr(loc), _stream(stream)))
+
+
+def csr_gather_rows(row_ptr, inc_ptr, inc, loc, max_row_len, A, vals, accumulate=False,
+                    stream=None):
+    """Atomic-free numeric assembly: vals[row r] (=|+=) sum of the element-matrix rows
+    inc[inc_ptr[r]:inc_ptr[r+1]] placed by loc (one warp per row, fixed order)."""
+    nrows, n = int(row_ptr.shape[0]) - 1, int(A.shape[-1])
+    _check(lib().femgpu_csr_gather_rows(nrows, n, _devptr(row_ptr), _devptr(inc_ptr), _devptr(inc),
+                                        _devptr(loc), int(max_row_len), _devptr(A), _devptr(vals),
+                                        int(accumulate), _stream(stream)))

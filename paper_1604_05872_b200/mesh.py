@@ -110,6 +110,17 @@ class GlobalMesh:
                 cols3[base + b * counts[seg] + pos_in_row] = cols + b * nn
         return row_ptr, cols3.astype(np.int32), 3 * nn
 
+    def row_incidence(self) -> tuple[np.ndarray, np.ndarray, int]:
+        """For the atomic-free assembly (femgpu_csr_gather_rows): inc_ptr int64
+        [ndofs+1] and inc int32 [E*n], the element-row ids e*n + j with dof_map[e][j]
+        == r for each global row r, in ascending id order; and the longest CSR row."""
+        dof, nd = self.dof_map()
+        flat = dof.reshape(-1)
+        inc = np.argsort(flat, kind="stable").astype(np.int32)
+        inc_ptr = np.concatenate([[0], np.cumsum(np.bincount(flat, minlength=nd))]).astype(np.int64)
+        row_ptr, _, _ = self.csr_pattern()
+        return inc_ptr, inc, int(np.diff(row_ptr).max())
+
     # -- host reference (test infrastructure for the scatter) -------------------
     def assemble_csr_host(self, A: np.ndarray, row_ptr: np.ndarray, col_idx: np.ndarray):
         """Sum of the element matrices into the CSR pattern, on the host (scipy)."""
@@ -165,23 +176,49 @@ class GlobalAssembler:
         femgpu.csr_positions(self.dof, self.row_ptr, self.col_idx, self.pos)
         self.vals = torch.zeros(col_idx.size, dtype=torch.float64, device=dev)
         self.form = form if form is not None else femgpu.Form.from_config(cfg)
+        self._rows = None
+
+    def row_plan(self):
+        """(inc_ptr, inc, loc, max_row_len) of the atomic-free row assembly, built once."""
+        if self._rows is None:
+            import torch
+
+            from . import femgpu
+
+            inc_ptr, inc, maxlen = self.mesh.row_incidence()
+            loc = torch.empty(self.pos.shape, dtype=torch.uint16, device=self.dev)
+            femgpu.csr_row_offsets(self.dof, self.row_ptr, self.pos, loc)
+            self._rows = (torch.from_numpy(inc_ptr).to(self.dev), torch.from_numpy(inc).to(self.dev),
+                          loc, maxlen)
+        return self._rows
 
     def gather(self, coef, stream=None):
         from . import femgpu
 
         femgpu.gather(self.V, self.cells, coef, self.coef_idx, self.coords, self.coeffs, stream)
 
-    def assemble(self, coef, stream=None, fused: bool = True):
+    def assemble(self, coef, stream=None, fused: bool = True, mode: str | None = None):
         """CSR values of the global matrix for global coefficient vector ``coef``.
-        ``fused``: element kernel and scatter in one launch (femgpu_assemble_csr);
-        otherwise A_e is materialised in ``self.A`` and scatter-added."""
+        ``mode`` (default from ``fused``): "fused" -- element kernel and scatter in one
+        call (femgpu_assemble_csr); "scatter" -- A_e materialised in ``self.A``, then
+        FP64-atomic scatter-add; "rows" -- A_e materialised, then the atomic-free
+        row-gather assembly (femgpu_csr_gather_rows; bit-reproducible)."""
         from . import femgpu
 
+        mode = mode or ("fused" if fused else "scatter")
         self.gather(coef, stream)
-        self.vals.zero_()
-        if fused:
+        if mode == "fused":
+            self.vals.zero_()
             self.form.assemble_csr(self.coords, self.coeffs, self.pos, self.vals, stream=stream)
-        else:
+        elif mode == "scatter":
+            self.vals.zero_()
             self.form.assemble(self.coords, self.coeffs, self.A, stream=stream)
             femgpu.scatter_add(self.A, self.pos, self.vals, stream)
+        elif mode == "rows":
+            inc_ptr, inc, loc, maxlen = self.row_plan()
+            self.form.assemble(self.coords, self.coeffs, self.A, stream=stream)
+            femgpu.csr_gather_rows(self.row_ptr, inc_ptr, inc, loc, maxlen, self.A, self.vals,
+                                   stream=stream)
+        else:
+            raise ValueError(f"unknown assembly mode {mode!r}")
         return self.vals

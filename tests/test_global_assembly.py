@@ -56,7 +56,99 @@ def test_csr_pattern_covers_element_matrices(name):
     assert np.isclose(v.sum(), A.sum())
 
 
+def row_gather_host(g, A, row_ptr, col_idx):
+    """The row-gather assembly's arithmetic on the host (test infrastructure):
+    for every row, zero, then add its incident element rows in inc order -- the
+    order femgpu_csr_gather_rows uses, so the sums are bit-identical."""
+    inc_ptr, inc, maxlen = g.row_incidence()
+    dof, nd = g.dof_map()
+    E, n = dof.shape
+    Ar = A.reshape(E * n, n)
+    # column -> offset inside the row (the symbolic step femgpu_csr_row_offsets does)
+    rows = dof.reshape(-1)
+    loc = np.empty((E * n, n), dtype=np.int64)
+    for t0 in range(0, E * n, 4096):
+        t = np.arange(t0, min(E * n, t0 + 4096))
+        cols = dof[t // n]                                     # [T][n] column dofs
+        for i, tt in enumerate(t):
+            b, e_ = row_ptr[rows[tt]], row_ptr[rows[tt] + 1]
+            loc[tt] = np.searchsorted(col_idx[b:e_], cols[i])
+    vals = np.zeros(col_idx.size)
+    cnt = np.diff(inc_ptr)
+    for s_ in range(int(cnt.max())):
+        r = np.nonzero(cnt > s_)[0]
+        t = inc[inc_ptr[r] + s_]
+        idx = row_ptr[r][:, None] + loc[t]
+        vals[idx] = vals[idx] + Ar[t]
+    return vals, maxlen
+
+
+@pytest.mark.parametrize("name", CONFIGS)
+def test_row_incidence_plan(name):
+    cfg = fe.CONFIGS[name]
+    g = mesh.GlobalMesh(cfg, N=2)
+    inc_ptr, inc, maxlen = g.row_incidence()
+    dof, nd = g.dof_map()
+    row_ptr, col_idx, _ = g.csr_pattern()
+    assert inc_ptr.size == nd + 1 and inc_ptr[-1] == dof.size
+    assert np.array_equal(np.sort(inc), np.arange(dof.size))        # every element row once
+    flat = dof.reshape(-1)
+    seg = np.repeat(np.arange(nd), np.diff(inc_ptr))
+    assert np.array_equal(flat[inc], seg)                            # row r's element rows
+    assert np.all(np.diff(inc)[np.diff(seg) == 0] > 0)               # ascending inside a row
+    assert maxlen == np.diff(row_ptr).max() <= 65536
+    # the row-gather arithmetic equals the scipy COO -> CSR sum
+    A = np.random.default_rng(1).uniform(-1, 1, size=(g.E, cfg.n, cfg.n))
+    got, _ = row_gather_host(g, A, row_ptr, col_idx)
+    ref = g.assemble_csr_host(A, row_ptr, col_idx)
+    assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
 # ----------------------------------------------------------------------------
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", CONFIGS)
+def test_row_gather_assembly(name):
+    # atomic-free assembly: bit-identical to the host sum in the plan's order,
+    # reproducible run to run, and += honoured
+    torch = pytest.importorskip("torch")
+    cfg = fe.CONFIGS[name]
+    ga = mesh.GlobalAssembler(cfg, N=3)
+    g = ga.mesh
+    coef = torch.from_numpy(g.global_coeffs()).to(ga.dev)
+    rows = ga.assemble(coef, mode="rows").clone()
+    again = ga.assemble(coef, mode="rows").clone()
+    torch.cuda.synchronize()
+    row_ptr, col_idx, _ = g.csr_pattern()
+    ref, _ = row_gather_host(g, ga.A.cpu().numpy(), row_ptr, col_idx)
+    assert np.array_equal(rows.cpu().numpy(), ref)
+    assert np.array_equal(again.cpu().numpy(), ref)
+    atomics = ga.assemble(coef, mode="scatter").clone()
+    torch.cuda.synchronize()
+    assert np.abs(atomics.cpu().numpy() - ref).max() <= 1e-13 * np.abs(ref).max()
+    from paper_1604_05872_b200 import femgpu
+
+    inc_ptr, inc, loc, maxlen = ga.row_plan()
+    acc = rows.clone()
+    femgpu.csr_gather_rows(ga.row_ptr, inc_ptr, inc, loc, maxlen, ga.A, acc, accumulate=True)
+    torch.cuda.synchronize()
+    assert np.array_equal(acc.cpu().numpy(), ref + ref)
+
+
+@pytest.mark.gpu
+def test_row_offsets_reject_entries_outside_their_row():
+    torch = pytest.importorskip("torch")
+    from paper_1604_05872_b200 import femgpu
+
+    cfg = fe.CONFIGS["c3"]
+    ga = mesh.GlobalAssembler(cfg, N=2)
+    pos = ga.pos.clone()
+    pos[0, 0, 0] = ga.row_ptr[-1].item() + 5   # outside row dof[0][0]
+    loc = torch.empty(pos.shape, dtype=torch.uint16, device=ga.dev)
+    with pytest.raises(femgpu.FemgpuError) as e:
+        femgpu.csr_row_offsets(ga.dof, ga.row_ptr, pos, loc)
+    assert e.value.code == 8
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", CONFIGS)
 def test_gather_assemble_scatter(name):

@@ -1,6 +1,7 @@
 #!/usr/bin/env python3
 """Global assembly pipeline on a config mesh: gather -> element kernel ->
-scatter-add into CSR.  Device-timed per phase with
+scatter-add into CSR: FP64-atomic scatter, the fused
+femgpu_assemble_csr, and the atomic-free row-gather assembly.  Device-timed per phase with
 CUDA events over K steps; setup (numbering, pattern, positions) timed once.
 usage: bench_global.py <cfg> [N] [steps]"""
 import json
@@ -54,6 +55,17 @@ def main():
         torch.cuda.synchronize()
         tf += ev[0].elapsed_time(ev[1])
     tf /= K
+    inc_ptr, inc, loc, maxlen = ga.row_plan()  # atomic-free row-gather assembly
+    tr = 0.0
+    for _ in range(K):
+        ev[0].record()
+        femgpu.csr_gather_rows(ga.row_ptr, inc_ptr, inc, loc, maxlen, ga.A, ga.vals)
+        ev[1].record()
+        torch.cuda.synchronize()
+        tr += ev[0].elapsed_time(ev[1])
+    tr /= K
+    nnz = int(ga.vals.numel())
+    r_bytes = E * n * n * (8 + 2) + E * n * 4 + nnz * 8  # A, loc, inc, vals written once
     ncoef = ga.coef_idx.shape[1]
     g_bytes = E * (4 * (4 + ncoef) + 8 * (12 + ncoef) + 8 * (12 + ncoef))  # idx + reads + writes
     s_bytes = E * n * n * (8 + 8 + 16)  # A, pos, atomic read-modify-write
@@ -64,6 +76,9 @@ def main():
         "total_ms": round(tg + ta + ts, 4), "elem_per_s": E / ((tg + ta + ts) / 1e3),
         "assemble_csr_ms": round(tf, 4), "fused_total_ms": round(tg + tf, 4),
         "fused_elem_per_s": E / ((tg + tf) / 1e3),
+        "gather_rows_ms": round(tr, 4), "rows_total_ms": round(tg + ta + tr, 4),
+        "rows_elem_per_s": E / ((tg + ta + tr) / 1e3), "gather_rows_GBs": r_bytes / (tr / 1e3) / 1e9,
+        "max_row_len": maxlen,
         "gather_GBs": g_bytes / (tg / 1e3) / 1e9, "scatter_GBs": s_bytes / (ts / 1e3) / 1e9,
         "kernel": ga.form.info["kernel_name"]}), flush=True)
 
