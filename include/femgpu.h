@@ -116,7 +116,9 @@ int femgpu_form_get_info(const femgpu_form* f, femgpu_form_info* info);
 /* Element matrices of cells [0, ncells) -- the hot path.  Device pointers
  * (cell-major layout above), stream = cudaStream_t (NULL = legacy default).
  * accumulate = 0 overwrites A; nonzero adds into it (the emitted-C `+=`
- * contract, emit_c.cpp:129).  Asynchronous: returns after enqueueing. */
+ * contract, emit_c.cpp:129).  Asynchronous: returns after enqueueing.  The
+ * current device must be the form's (FEMGPU_ERR_INVALID_ARG otherwise).  Safe
+ * to call from several host threads at once, including their first calls. */
 int femgpu_assemble(const femgpu_form* f, long ncells, const double* coords,
                     const double* coeffs, double* A, int accumulate, void* stream);
 

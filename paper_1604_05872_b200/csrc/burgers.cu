@@ -688,15 +688,23 @@ cudaError_t launch_burgers(int ns, long E, const double* coords, const double* c
   if (ns != bz::NS) return cudaErrorInvalidValue;
   if (E <= 0) return cudaSuccess;
   if (E > 0x7fffffffL) return cudaErrorInvalidValue;
-  static bool configured = false;
-  if (!configured) {
+  static const char once_key = 0;  // one per (kernel instantiation, device)
+  const cudaError_t e0 = once_per_device(&once_key, [&]() -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(burgers_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)bz::SMEM);
     if (e != cudaSuccess) return e;
-    configured = true;
-  }
+    return cudaSuccess;
+  });
+  if (e0 != cudaSuccess) return e0;
   auto encode = encode_fn();
   if (!encode) return cudaErrorNotSupported;
+  // cuTensorMapEncodeTiled is a driver call: it needs the device's context current in
+  // THIS host thread, which a thread whose first CUDA call is this launch does not have
+  // yet (tests/test_gpu_robust.py::test_first_launch_race_fresh_process)
+  int dev = 0;
+  cudaError_t ec = cudaGetDevice(&dev);
+  if (ec == cudaSuccess) ec = cudaSetDevice(dev);
+  if (ec != cudaSuccess) return ec;
   // A_e as a 3D tensor [E][60 rows][60 cols]; box = one (c,d) block of 16 cells
   CUtensorMap map;
   const cuuint64_t dims[3] = {(cuuint64_t)bz::N, (cuuint64_t)bz::N, (cuuint64_t)E};

@@ -12,6 +12,7 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <set>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -319,6 +320,19 @@ void launch(const femgpu_form* f, long E, const double* coords, const double* co
 
 namespace femgpu {
 void set_last_error(const std::string& m) { g_last_error = m; }
+
+cudaError_t once_per_device(const void* key, const std::function<cudaError_t()>& init) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  const cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({key, dev})) return cudaSuccess;
+  const cudaError_t r = init();
+  if (r == cudaSuccess) done.insert({key, dev});
+  return r;
+}
 }  // namespace femgpu
 
 extern "C" {
@@ -452,6 +466,9 @@ int femgpu_assemble(const femgpu_form* f, long ncells, const double* coords, con
     check_ptr(coords, "coords");
     check_ptr(A, "A");
     if (f->ncoef > 0) check_ptr(coeffs, "coeffs");
+    int cur = 0;  // the form's tables live on the device it was created on
+    cuda_check(cudaGetDevice(&cur), "cudaGetDevice");
+    if (cur != f->device) throw Error(FEMGPU_ERR_INVALID_ARG, "form belongs to another device");
     launch(f, ncells, coords, coeffs, A, accumulate, static_cast<cudaStream_t>(stream));
   });
 }

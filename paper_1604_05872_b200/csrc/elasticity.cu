@@ -370,8 +370,8 @@ void elas_tensor_tables(int nq, const double* W, const double* D, const double* 
 cudaError_t launch_elas_tensor(long E, const double* coords, const double* coef, const double* tab,
                                double* A, int acc, cudaStream_t s) {
   if (E <= 0) return cudaSuccess;
-  static bool configured = false;
-  if (!configured) {
+  static const char once_key = 0;  // one per (kernel instantiation, device)
+  const cudaError_t e0 = once_per_device(&once_key, [&]() -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(elas_tensor_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)et::SMEM);
     if (e != cudaSuccess) return e;
@@ -379,8 +379,9 @@ cudaError_t launch_elas_tensor(long E, const double* coords, const double* coef,
     et_sym_table(sym);
     e = cudaMemcpyToSymbol(c_et_sym, sym, sizeof sym);
     if (e != cudaSuccess) return e;
-    configured = true;
-  }
+    return cudaSuccess;
+  });
+  if (e0 != cudaSuccess) return e0;
   const long ntiles = (E + et::CELLS - 1) / et::CELLS;
   const long maxc = (long)et::CTAS_PER_SM * kNumSMs;
   const int grid = (int)(ntiles < maxc ? ntiles : maxc);

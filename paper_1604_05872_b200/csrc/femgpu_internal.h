@@ -4,12 +4,19 @@
 #include <cuda_runtime.h>
 #include <stddef.h>
 
+#include <functional>
 #include <string>
 
 namespace femgpu {
 
 // The thread-local message femgpu_last_error() returns (capi.cu).
 void set_last_error(const std::string& message);
+
+// Runs init() once per (key, current device) -- kernel attributes and __constant__
+// tables live in each device's context -- under a process-wide lock, so concurrent
+// first launches from several host threads never race a launch past the setup.
+// Only a successful init is remembered.
+cudaError_t once_per_device(const void* key, const std::function<cudaError_t()>& init);
 
 // Pre-evaluated P1 Helmholtz tables (kernel parameters: constant bank).
 struct HelmP1Params {

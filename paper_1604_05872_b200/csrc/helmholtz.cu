@@ -170,15 +170,16 @@ cudaError_t launch_helm_p1(const HelmP1Params& prm, long E, const double* coords
                            const double* coef, double* A, int acc, cudaStream_t s,
                            const long* pos, double* vals) {
   if (E <= 0) return cudaSuccess;
-  static bool configured = false;
-  if (!configured) {
+  static const char once_key = 0;  // one per (kernel instantiation, device)
+  const cudaError_t e0 = once_per_device(&once_key, [&]() -> cudaError_t {
     for (auto fn : {helm_p1_kernel<false>, helm_p1_kernel<true>}) {
       cudaError_t e =
           cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P1_SMEM);
       if (e != cudaSuccess) return e;
     }
-    configured = true;
-  }
+    return cudaSuccess;
+  });
+  if (e0 != cudaSuccess) return e0;
   const long ntiles = (E + P1_TILE - 1) / P1_TILE;
   const long maxc = (long)P1_CTAS * kNumSMs;
   const int grid = (int)(ntiles < maxc ? ntiles : maxc);
@@ -483,13 +484,14 @@ template <int NS, int NC>
 static cudaError_t launch_tensor_t(long E, const double* coords, const double* coef,
                                    const double* Sfrag, double* A, int acc, cudaStream_t s) {
   using Sh = HelmTensorShape<NS, NC>;
-  static bool configured = false;
-  if (!configured) {
+  static const char once_key = 0;  // one per (kernel instantiation, device)
+  const cudaError_t e0 = once_per_device(&once_key, [&]() -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(helm_tensor_kernel<NS, NC>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::SMEM);
     if (e != cudaSuccess) return e;
-    configured = true;
-  }
+    return cudaSuccess;
+  });
+  if (e0 != cudaSuccess) return e0;
   const long ntiles = (E + Sh::CELLS - 1) / Sh::CELLS;
   const long max_ctas = kNumSMs;  // persistent: one warp-specialised CTA per SM
   const int grid = (int)(ntiles < max_ctas ? ntiles : max_ctas);

@@ -485,7 +485,6 @@ struct Kernel {
   std::vector<char> cubin;
   cudaLibrary_t lib = nullptr;
   cudaKernel_t kern = nullptr;
-  int device = -1;
 
   long size_of(const std::string& name, long ncells) const {
     long s = 1;
@@ -902,13 +901,12 @@ void cuda_ok(cudaError_t e, const char* what) {
 cudaKernel_t loaded(femgpu_ir* f) {
   std::lock_guard<std::mutex> lock(f->mu);
   auto& K = *f->k;
-  int dev = 0;
-  cuda_ok(cudaGetDevice(&dev), "cudaGetDevice");
-  if (!K.kern || K.device != dev) {
+  // a cudaLibrary is context-independent: one load serves every device (the module
+  // is loaded into a device's context on that device's first launch)
+  if (!K.kern) {
     cuda_ok(cudaLibraryLoadData(&K.lib, K.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0),
             "cudaLibraryLoadData");
     cuda_ok(cudaLibraryGetKernel(&K.kern, K.lib, K.fn.c_str()), "cudaLibraryGetKernel");
-    K.device = dev;
   }
   return K.kern;
 }

@@ -941,13 +941,14 @@ static cudaError_t launch_svk_ws(long E, const double* coords, const double* coe
                                  const double* tab, double* A, int acc, cudaStream_t s) {
   using Sh = SvkWsShape<NS, Q>;
   auto kern = pair_svk_ws_kernel<NS, Q>;
-  static bool configured = false;
-  if (!configured) {
+  static const char once_key = 0;  // one per (kernel instantiation, device)
+  const cudaError_t e0 = once_per_device(&once_key, [&]() -> cudaError_t {
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::SMEM);
     if (e != cudaSuccess) return e;
-    configured = true;
-  }
+    return cudaSuccess;
+  });
+  if (e0 != cudaSuccess) return e0;
   const long ntiles = (E + Sh::CELLS - 1) / Sh::CELLS;
   const long maxc = (long)Sh::CTAS_PER_SM * kNumSMs;
   const int grid = (int)(ntiles < maxc ? ntiles : maxc);
@@ -961,13 +962,14 @@ static cudaError_t launch_pair_t(long E, const double* coords, const double* coe
   using Sh = PairShape<KIND, NS, Q>;
   if constexpr (Sh::SVK && PAIR_SVK_WS) return launch_svk_ws<NS, Q>(E, coords, coef, tab, A, acc, s);
   auto kern = (Sh::SVK || Sh::FLAT) ? pair_flat_kernel<KIND, NS, Q> : pair_ws_kernel<NS, Q>;
-  static bool configured = false;
-  if (!configured) {
+  static const char once_key = 0;  // one per (kernel instantiation, device)
+  const cudaError_t e0 = once_per_device(&once_key, [&]() -> cudaError_t {
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sh::SMEM);
     if (e != cudaSuccess) return e;
-    configured = true;
-  }
+    return cudaSuccess;
+  });
+  if (e0 != cudaSuccess) return e0;
   const long ntiles = (E + Sh::CELLS - 1) / Sh::CELLS;
   const long maxc = (long)Sh::CTAS_PER_SM * kNumSMs;
   const int grid = (int)(ntiles < maxc ? ntiles : maxc);

@@ -106,3 +106,57 @@ def test_concurrent_streams_and_threads():
         t.join()
     assert set(results) == set(CONFIGS)
     assert max(results.values()) < TOL, results
+
+
+_FIRST_LAUNCH_RACE = r"""
+import sys, threading
+import numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_1604_05872_b200 import fe, femgpu
+dev = torch.device("cuda:0")
+torch.cuda.init()
+jobs = []
+for name in ("c1", "c2", "c3", "c4", "c5"):
+    cfg = fe.CONFIGS[name]
+    coords, coeffs = fe.cell_inputs(cfg, ncells=97)
+    x = torch.from_numpy(coords).to(dev)
+    c = torch.from_numpy(coeffs).to(dev)
+    for _ in range(4):  # four threads per kernel race its first launch
+        form = femgpu.Form.from_config(cfg)
+        out = torch.empty((97, cfg.n, cfg.n), dtype=torch.float64, device=dev)
+        jobs.append((name, form, x, c, out))
+torch.cuda.synchronize()
+gate = threading.Barrier(len(jobs))
+errors = []
+def run(job):
+    name, form, x, c, out = job
+    s = torch.cuda.Stream(device=dev)
+    gate.wait()
+    try:
+        form.assemble(x, c, out, stream=s.cuda_stream)
+        s.synchronize()
+    except Exception as e:  # noqa: BLE001
+        errors.append(f"{name}: {e}")
+threads = [threading.Thread(target=run, args=(j,)) for j in jobs]
+for t in threads: t.start()
+for t in threads: t.join()
+assert not errors, errors
+for name in ("c1", "c2", "c3", "c4", "c5"):
+    outs = [j[4].cpu().numpy() for j in jobs if j[0] == name]
+    assert all(np.array_equal(outs[0], o) for o in outs[1:]), name
+print("ok")
+"""
+
+
+def test_first_launch_race_fresh_process():
+    # the per-(kernel, device) setup (dynamic shared memory attribute, __constant__
+    # tables) must be complete before any thread's first launch: a fresh process,
+    # 20 threads released together into their first assemble call
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _FIRST_LAUNCH_RACE, root], capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
