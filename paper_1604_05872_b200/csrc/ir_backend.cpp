@@ -334,6 +334,10 @@ struct Emitter {
   std::set<const Node*> dist;
   std::set<std::string> shared;
   bool in_J = false;
+  // warp mapping: baked (pre-evaluated) tables with a dimension named J are stored
+  // with that dimension innermost, so the lanes' reads T[..][j=lane][..] are
+  // consecutive addresses (femopt's row-major [j][k] layout strides them by n_k)
+  std::map<std::string, std::vector<size_t>> perm;  // stored position -> IR position
 
   std::string temp_ref(const std::string& name, const std::string& flat) const {
     if (shared.count(name)) return "s_" + ident(name) + "[w_][" + flat + "]";
@@ -347,8 +351,11 @@ struct Emitter {
     const auto& dd = dims.at(name);
     if (idx.size() != dd.size()) irfail(name + " subscripted with the wrong rank");
     if (idx.empty()) return "0";
-    std::string e = "(long)i_" + idx[0];
-    for (size_t i = 1; i < dd.size(); ++i) e = "(" + e + " * " + ext_of(dd[i]) + " + i_" + idx[i] + ")";
+    auto it = perm.find(name);
+    auto at = [&](size_t i) { return it == perm.end() ? i : it->second[i]; };
+    std::string e = "(long)i_" + idx[at(0)];
+    for (size_t i = 1; i < dd.size(); ++i)
+      e = "(" + e + " * " + ext_of(dd[at(i)]) + " + i_" + idx[at(i)] + ")";
     return e;
   }
   std::string temp_flat(const std::string& name, const std::vector<std::string>& idx) const {
@@ -705,6 +712,17 @@ std::unique_ptr<Kernel> generate(const char* json, int strategy) {
     const Json* pv = kv.second->get("provenance");
     const bool pre = pv && pv->kind == Json::Str && pv->str == "preevaluated";
     (pre ? K->preevaluated : K->inputs).push_back(kv.first);
+    if (pre && warp) {
+      const auto& dd = em.dims.at(kv.first);
+      auto j = std::find(dd.begin(), dd.end(), em.J);
+      if (j != dd.end() && j + 1 != dd.end()) {
+        std::vector<size_t> order;
+        for (size_t i = 0; i < dd.size(); ++i)
+          if (i != (size_t)(j - dd.begin())) order.push_back(i);
+        order.push_back(j - dd.begin());
+        em.perm[kv.first] = order;
+      }
+    }
   }
   K->outputs.assign(em.outs.begin(), em.outs.end());
   K->constants.assign(em.consts.begin(), em.consts.end());
@@ -761,9 +779,27 @@ std::unique_ptr<Kernel> generate(const char* json, int strategy) {
   for (const auto& name : K->preevaluated) {
     const Json& vals = tables[name]->at("values");
     src += "__device__ const double t_" + ident(name) + "[" + std::to_string(std::max<size_t>(1, vals.arr.size())) + "] = {";
+    auto pit = em.perm.find(name);
+    std::vector<long> ex, stride;  // IR (row-major) extents and strides
+    if (pit != em.perm.end()) {
+      for (const auto& d : em.dims.at(name)) ex.push_back(em.ext.at(d));
+      stride.assign(ex.size(), 1);
+      for (size_t i = ex.size() - 1; i > 0; --i) stride[i - 1] = stride[i] * ex[i];
+    }
     for (size_t i = 0; i < vals.arr.size(); ++i) {
       if (i) src += ",";
-      src += lit(vals.arr[i].num);
+      size_t src_i = i;
+      if (pit != em.perm.end()) {  // stored flat index i -> IR flat index
+        const auto& ord = pit->second;
+        size_t rem = i, k = 0;
+        for (size_t a = ord.size(); a-- > 0;) {
+          const long c = (long)(rem % ex[ord[a]]);
+          rem /= ex[ord[a]];
+          k += c * stride[ord[a]];
+        }
+        src_i = k;
+      }
+      src += lit(vals.arr[src_i].num);
     }
     src += "};\n";
   }
