@@ -122,6 +122,17 @@ int femgpu_form_get_info(const femgpu_form* f, femgpu_form_info* info);
 int femgpu_assemble(const femgpu_form* f, long ncells, const double* coords,
                     const double* coeffs, double* A, int accumulate, void* stream);
 
+/* Element VECTORS of the form's family (arity-1 nests, kernel.cpp:369-390; the
+ * IR paper_1604_05872_b200/ir.py builds with build_vector), same tables, inputs
+ * and conventions as femgpu_assemble, output b [E][n]:
+ *   HELMHOLTZ        load vector        b_j     = int f phi_j
+ *   HYPERELASTICITY  internal work      r_(c,j) = int (F S) : grad(phi_j e_c)
+ *   BURGERS          residual           r_(c,j) = int (u_c/dt + (u.grad)u_c) phi_j
+ *                                                 + nu grad u_c . grad phi_j
+ * FEMGPU_ERR_UNSUPPORTED for ELASTICITY and for sizes without a kernel. */
+int femgpu_assemble_vector(const femgpu_form* f, long ncells, const double* coords,
+                           const double* coeffs, double* b, int accumulate, void* stream);
+
 /* Same, from and to HOST memory: copies in, assembles and copies out in a
  * chunked multi-stream pipeline (the end-to-end path).  Synchronous.
  * Pinned host buffers give full PCIe bandwidth; pageable ones work too. */

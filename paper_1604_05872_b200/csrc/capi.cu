@@ -75,6 +75,7 @@ struct femgpu_form {
   femgpu::HelmP1Params p1{};
   double* d_tab = nullptr;
   size_t tab_doubles = 0;
+  double* d_vtab = nullptr;  // element-vector tables (femgpu_assemble_vector), if supported
   double flops_per_cell = 0;
   int kernels_per_launch = 1;
   std::string kernel_name;
@@ -95,6 +96,7 @@ struct femgpu_form {
     cudaGetDevice(&cur);
     cudaSetDevice(device);
     if (d_tab) cudaFree(d_tab);
+    if (d_vtab) cudaFree(d_vtab);
     if (csr_scratch) cudaFree(csr_scratch);
     for (int i = 0; i < NSTREAM; ++i) {
       if (host_buf[i]) cudaFree(host_buf[i]);
@@ -430,6 +432,33 @@ int femgpu_form_create(const femgpu_form_desc* d, femgpu_form** out) {
                             cudaMemcpyHostToDevice),
                  "cudaMemcpy(tables)");
     }
+    if (femgpu::vector_supported(f->kind, f->ns, f->nc)) {
+      // element-vector tables (vector.cu): Helmholtz M_jm = sum_q W_q B_qj P_qm (ascending
+      // q, preeval.cpp:269-274); SVK W | D | P; Burgers W | B | D
+      std::vector<double> v;
+      const int Q = f->nq, ns = f->ns, nc = f->nc;
+      if (f->kind == FEMGPU_HELMHOLTZ) {
+        v.assign((size_t)ns * nc, 0.0);
+        for (int j = 0; j < ns; ++j)
+          for (int m = 0; m < nc; ++m) {
+            double s = 0.0;
+            for (int q = 0; q < Q; ++q)
+              s += f->W[q] * f->B[(size_t)q * ns + j] * f->P[(size_t)q * nc + m];
+            v[(size_t)j * nc + m] = s;
+          }
+      } else if (f->kind == FEMGPU_HYPERELASTICITY) {
+        v.insert(v.end(), f->W.begin(), f->W.end());
+        v.insert(v.end(), f->D.begin(), f->D.end());
+        v.insert(v.end(), f->P.begin(), f->P.end());
+      } else {
+        v.insert(v.end(), f->W.begin(), f->W.end());
+        v.insert(v.end(), f->B.begin(), f->B.end());
+        v.insert(v.end(), f->D.begin(), f->D.end());
+      }
+      cuda_check(cudaMalloc(&f->d_vtab, v.size() * sizeof(double)), "cudaMalloc(vector tables)");
+      cuda_check(cudaMemcpy(f->d_vtab, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice),
+                 "cudaMemcpy(vector tables)");
+    }
     build_argv_names(f.get());
     *out = f.release();
   });
@@ -470,6 +499,29 @@ int femgpu_assemble(const femgpu_form* f, long ncells, const double* coords, con
     cuda_check(cudaGetDevice(&cur), "cudaGetDevice");
     if (cur != f->device) throw Error(FEMGPU_ERR_INVALID_ARG, "form belongs to another device");
     launch(f, ncells, coords, coeffs, A, accumulate, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int femgpu_assemble_vector(const femgpu_form* f, long ncells, const double* coords,
+                           const double* coeffs, double* b, int accumulate, void* stream) {
+  if (!f) {
+    g_last_error = "null form";
+    return FEMGPU_ERR_INVALID_ARG;
+  }
+  return guarded([&] {
+    if (ncells < 0) throw Error(FEMGPU_ERR_INVALID_ARG, "negative cell count");
+    if (!f->d_vtab)
+      throw Error(FEMGPU_ERR_UNSUPPORTED, "no element-vector kernel for this form");
+    if (ncells == 0) return;
+    check_ptr(coords, "coords");
+    check_ptr(b, "b");
+    if (f->ncoef > 0) check_ptr(coeffs, "coeffs");
+    int cur = 0;
+    cuda_check(cudaGetDevice(&cur), "cudaGetDevice");
+    if (cur != f->device) throw Error(FEMGPU_ERR_INVALID_ARG, "form belongs to another device");
+    cuda_check(femgpu::launch_vector(f->kind, f->nq, f->ns, f->nc, ncells, coords, coeffs, f->d_vtab,
+                                     f->consts, b, accumulate, static_cast<cudaStream_t>(stream)),
+               "element-vector kernel");
   });
 }
 

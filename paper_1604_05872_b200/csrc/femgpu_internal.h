@@ -68,6 +68,12 @@ cudaError_t launch_csr_gather_rows(long nrows, int n, int maxlen, const long* ro
 
 // Burgers tensor schedule (see burgers.cu).
 bool burgers_supported(int nq, int ns);
+
+// element vectors (vector.cu)
+bool vector_supported(int kind, int ns, int nc);
+cudaError_t launch_vector(int kind, int nq, int ns, int nc, long E, const double* coords,
+                          const double* coef, const double* tab, const double* consts, double* out,
+                          int acc, cudaStream_t s);
 size_t burgers_table_doubles();
 // Returns the derivative-space rank used by GEMM-1, or -1 if unsupported.
 int burgers_tables(int nq, const double* W, const double* B, const double* D, double* out);

@@ -39,6 +39,7 @@ ERROR_NAMES = {
 
 # Every symbol include/femgpu.h declares (checked by tests/test_abi.py).
 EXPORTS = ("femgpu_form_create", "femgpu_form_free", "femgpu_form_get_info", "femgpu_assemble",
+           "femgpu_assemble_vector",
            "femgpu_assemble_host", "femgpu_kernel_argv", "femgpu_kernel_argc",
            "femgpu_kernel_argname", "femgpu_gather", "femgpu_csr_positions",
            "femgpu_scatter_add", "femgpu_csr_row_offsets", "femgpu_csr_gather_rows", "femgpu_assemble_csr", "femgpu_ir_create", "femgpu_ir_free", "femgpu_ir_get_info",
@@ -85,6 +86,7 @@ def lib():
         L.femgpu_form_free.restype = None
         L.femgpu_form_get_info.argtypes = [vp, C.POINTER(FormInfo)]
         L.femgpu_assemble.argtypes = [vp, C.c_long, vp, vp, vp, C.c_int, vp]
+        L.femgpu_assemble_vector.argtypes = [vp, C.c_long, vp, vp, vp, C.c_int, vp]
         L.femgpu_assemble_host.argtypes = [vp, C.c_long, dp, dp, dp, C.c_int]
         L.femgpu_kernel_argv.argtypes = [vp, C.c_long, C.POINTER(dp), C.POINTER(dp), dp]
         L.femgpu_kernel_argc.argtypes = [vp, C.c_int, C.POINTER(C.c_int)]
@@ -170,6 +172,15 @@ class Form:
         s = None if stream is None else (stream if isinstance(stream, int) else stream.cuda_stream)
         _check(lib().femgpu_assemble(self.h, E, _devptr(coords), _devptr(coeffs), _devptr(out),
                                      int(accumulate), s))
+
+    def assemble_vector(self, coords, coeffs, out, ncells: int | None = None,
+                        accumulate: bool = False, stream=None):
+        """Element vectors [E][n] of the form's family into ``out`` (device tensors):
+        Helmholtz load, St Venant--Kirchhoff / Burgers residual (femgpu_assemble_vector)."""
+        E = int(coords.shape[0]) if ncells is None else int(ncells)
+        s = None if stream is None else (stream if isinstance(stream, int) else stream.cuda_stream)
+        _check(lib().femgpu_assemble_vector(self.h, E, _devptr(coords), _devptr(coeffs),
+                                            _devptr(out), int(accumulate), s))
 
     def assemble_csr(self, coords, coeffs, pos, vals, ncells: int | None = None, stream=None):
         """Element matrices straight into CSR values: vals[pos] += A_e (device tensors;

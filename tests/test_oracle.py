@@ -79,6 +79,25 @@ def test_port_vs_live_reference_interpreter(name):
     assert frob_rel(port.assemble(cfg, tabs, coords, coeffs), R) < 1e-13
 
 
+@pytest.mark.skipif(not os.path.exists(os.path.join(os.path.dirname(port.HERE), "oracle", "_ref",
+                                                    "libfemopt_ref.so")),
+                    reason="reference oracle not built (needs /root/reference)")
+@pytest.mark.parametrize("name", ["c1", "c2", "c4", "c5"])
+def test_vector_port_vs_live_reference_interpreter(name):
+    # the element-vector oracle (port.assemble_vector) against the reference's own
+    # interpreter (interp.cpp:125-154) on the arity-1 IR of the same form
+    import refbridge as rb
+
+    cfg = fe.CONFIGS[name]
+    tabs = fe.tables(cfg)
+    coords, coeffs = fe.cell_inputs(cfg, ncells=3, shard=5)
+    oname, k = ir.build_vector(cfg, coords, coeffs, tabs)
+    R = np.asarray(rb.interpret(ir.dumps(k), oname)).reshape(3, -1)
+    V = port.assemble_vector(cfg, tabs, coords, coeffs)
+    assert V.shape == R.shape
+    assert frob_rel(V, R) < 1e-13
+
+
 def test_reference_acceptance_suite():
     """The reference's own acceptance binary (proj/tests/acceptance.cpp) passes."""
     import subprocess

@@ -12,7 +12,7 @@ flop_count of the IR that runs (kernel.cpp:521) -- for the optimized plans that
 is the reference's F_alg, so the rate compares directly with the reference's
 CPU rate on the same kernel (bench.py --impl reference).  The hand-written
 kernels (bench.py) are the fast path.
-usage: bench_generic.py [--raw] [--femopt] [cfg ...]"""
+usage: bench_generic.py [--raw] [--femopt] [--vectors] [cfg ...]"""
 import argparse
 import gzip
 import json
@@ -63,10 +63,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--raw", action="store_true")
     ap.add_argument("--femopt", action="store_true")
+    ap.add_argument("--vectors", action="store_true",
+                    help="the element-vector forms (ir.build_vector: load / residuals), raw IR")
     ap.add_argument("--strategy", default="auto", choices=["auto", "thread", "warp"])
     ap.add_argument("configs", nargs="*", default=["c1", "c2", "c3", "c4", "c5"])
     a = ap.parse_args()
-    if not (a.raw or a.femopt):
+    if not (a.raw or a.femopt or a.vectors):
         a.raw = a.femopt = True
     dev = torch.device("cuda:0")
     for name in a.configs:
@@ -79,6 +81,10 @@ def main():
             tabs = fe.tables(cfg)
             c4, f4 = fe.cell_inputs(cfg, ncells=4)
             jobs.append(("raw (ufl)", [k for _, k in ir.build(cfg, c4, f4, tabs=tabs)], None))
+        if a.vectors and name != "c3":
+            tabs = fe.tables(cfg)
+            c4, f4 = fe.cell_inputs(cfg, ncells=4)
+            jobs.append(("raw vector", [ir.build_vector(cfg, c4, f4, tabs=tabs)[1]], None))
         if a.femopt:
             for fn in sorted(os.listdir(IR_FULL)) if os.path.isdir(IR_FULL) else []:
                 if fn.startswith(name + "_") and fn.endswith(".json.gz"):
@@ -91,6 +97,8 @@ def main():
             line = {"config": name, "cells": E, "ir": label, "kernels": len(kernels),
                     "strategy": sorted(set(strategies)), "ms": round(ms, 3),
                     "elem_per_s": E / (ms / 1e3)}
+            if label == "raw vector":  # inputs + the element vector, FP64
+                line["hbm_gbs"] = round(E * 8 * (12 + cfg.ncoef + cfg.n) / (ms / 1e3) / 1e9, 1)
             if fpc:
                 line["ir_flops_per_cell"] = fpc
                 line["ir_gflops"] = round(E * fpc / (ms / 1e3) / 1e9, 1)
