@@ -434,7 +434,7 @@ int femgpu_form_create(const femgpu_form_desc* d, femgpu_form** out) {
     }
     if (femgpu::vector_supported(f->kind, f->ns, f->nc)) {
       // element-vector tables (vector.cu): Helmholtz M_jm = sum_q W_q B_qj P_qm (ascending
-      // q, preeval.cpp:269-274); SVK W | D | P; Burgers W | B | D
+      // q, preeval.cpp:269-274); SVK W | D | P; Burgers W | B | D_a (padded, vector.cu)
       std::vector<double> v;
       const int Q = f->nq, ns = f->ns, nc = f->nc;
       if (f->kind == FEMGPU_HELMHOLTZ) {
@@ -450,10 +450,17 @@ int femgpu_form_create(const femgpu_form_desc* d, femgpu_form** out) {
         v.insert(v.end(), f->W.begin(), f->W.end());
         v.insert(v.end(), f->D.begin(), f->D.end());
         v.insert(v.end(), f->P.begin(), f->P.end());
-      } else {
-        v.insert(v.end(), f->W.begin(), f->W.end());
-        v.insert(v.end(), f->B.begin(), f->B.end());
-        v.insert(v.end(), f->D.begin(), f->D.end());
+      } else {  // W[Qp] | T[4][Qp][ns], T_0 = B, T_{1+a} = D_a, zero rows past Q
+        const int Qp = femgpu::vector_table_qpad(Q);
+        v.assign((size_t)Qp + 4 * (size_t)Qp * ns, 0.0);
+        for (int q = 0; q < Q; ++q) {
+          v[q] = f->W[q];
+          for (int j = 0; j < ns; ++j) {
+            v[Qp + (size_t)q * ns + j] = f->B[(size_t)q * ns + j];
+            for (int a = 0; a < 3; ++a)
+              v[Qp + ((size_t)(1 + a) * Qp + q) * ns + j] = f->D[((size_t)a * Q + q) * ns + j];
+          }
+        }
       }
       cuda_check(cudaMalloc(&f->d_vtab, v.size() * sizeof(double)), "cudaMalloc(vector tables)");
       cuda_check(cudaMemcpy(f->d_vtab, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice),

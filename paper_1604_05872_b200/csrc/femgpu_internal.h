@@ -71,6 +71,7 @@ bool burgers_supported(int nq, int ns);
 
 // element vectors (vector.cu)
 bool vector_supported(int kind, int ns, int nc);
+int vector_table_qpad(int nq);  // Burgers residual: quadrature rows padded to its chunk
 cudaError_t launch_vector(int kind, int nq, int ns, int nc, long E, const double* coords,
                           const double* coef, const double* tab, const double* consts, double* out,
                           int acc, cudaStream_t s);

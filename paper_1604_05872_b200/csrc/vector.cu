@@ -34,9 +34,17 @@ constexpr int VEC_THREADS = 128;
 
 __device__ __forceinline__ double ldro(const double* p) { return __ldg(p); }
 
-// coalesced copy of `rows` rows of `w` doubles (contiguous in global) into padded smem rows
+// coalesced copy of `rows` rows of `w` doubles (contiguous in global) into padded smem
+// rows, as asynchronous copies (cp.async: every element of the CTA's range in flight at
+// once, no register round trip); stage_wait() + __syncthreads() before use
 __device__ __forceinline__ void stage_rows(double* s, int stride, const double* g, int rows, int w) {
-  for (int i = threadIdx.x; i < rows * w; i += blockDim.x) s[(i / w) * stride + i % w] = g[i];
+  for (int i = threadIdx.x; i < rows * w; i += blockDim.x)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(&s[(i / w) * stride + i % w])),
+                 "l"(g + i)
+                 : "memory");
+}
+__device__ __forceinline__ void stage_wait() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 __device__ __forceinline__ void store_rows(double* g, const double* s, int stride, int rows, int w,
                                            int acc) {
@@ -89,6 +97,7 @@ __global__ void __launch_bounds__(VEC_THREADS) vec_helm_kernel(long E, const dou
     }
   stage_rows(sx, XS, coords + c0 * 12, nt, 12);
   stage_rows(sf, FS, coef + c0 * NC, nt, NC);
+  stage_wait();
   __syncthreads();
   {
     const int t = threadIdx.x;
@@ -138,12 +147,6 @@ __global__ void __launch_bounds__(VEC_THREADS) vec_helm_kernel(long E, const dou
 #ifndef VEC_SVK_MINB
 #define VEC_SVK_MINB 2  // CTAs per SM the SVK residual kernel is register-capped for
 #endif
-#ifndef VEC_BZ_MUNROLL
-#define VEC_BZ_MUNROLL 20
-#endif
-#ifndef VEC_BZ_MINB
-#define VEC_BZ_MINB 1
-#endif
 template <int NS>
 __global__ void __launch_bounds__(VEC_THREADS, VEC_SVK_MINB) vec_svk_kernel(long E, int Q,
                                                               const double* __restrict__ coords,
@@ -163,6 +166,7 @@ __global__ void __launch_bounds__(VEC_THREADS, VEC_SVK_MINB) vec_svk_kernel(long
   const int nt = (int)min((long)CELLS, E - c0);
   stage_rows(sx, XS, coords + c0 * 12, nt, 12);
   stage_rows(sc, CS, coef + c0 * NCOEF, nt, NCOEF);
+  stage_wait();
   __syncthreads();
   const int t = threadIdx.x;
   double rc[3][NS];
@@ -257,74 +261,146 @@ __global__ void __launch_bounds__(VEC_THREADS, VEC_SVK_MINB) vec_svk_kernel(long
 }
 
 // ---------------------------------------------------------------------------
-// Burgers residual, vector P_k: thread per (cell, component c), warp = c, lane = cell
-// tab: W[Q] | B[Q][NS] | D[3][Q][NS];  coeffs: u (3 x NS)
+// Burgers residual, vector P3: two FP64 tensor-core GEMMs per 16-cell tile and chunk
+// of BZQ = 6 quadrature points (the quadrature schedule of sharing.cpp:409-607 with
+// its two contractions on DMMA).  Rows = (component c, cell): m16 tile c.
+//   A:  V[(c,e)][(q,s)] = sum_m u_{e,c,m} T_s[q][m]      T_0 = B, T_{1+a} = D_a
+//       -> u_c(q), reference gradient of u_c at q             (K = 20, N = 6 x 4)
+//   B:  per (cell, q), in place: adv_c = wq (u_c/dt + u . grad u_c),
+//       t_ca = wq nu sum_b K_ab (grad u_c)_b,  wq = W_q |det|
+//   C:  r[(c,e)][j] += sum_(q,s) Y[(c,e)][(q,s)] T_s[q][j]    (K = 6 x 4, N = 20 -> 24)
+// 3 warps: phase A warp w computes n-tile w (2 points x 4 tables) of all 3 m-tiles
+// (the u fragments of the tile live in registers); phase B one thread per (cell,
+// point); phase C warp w owns component w's 3 output n-tiles for the whole tile.
+// tab: W[Qp] | T[4][Qp][NS] (Qp = Q rounded up to BZQ, zero rows past Q).
 // ---------------------------------------------------------------------------
-constexpr int kBzMUnroll = VEC_BZ_MUNROLL;
+constexpr int BZQ = 6;
+constexpr int bz_qpad(int Q) { return (Q + BZQ - 1) / BZQ * BZQ; }
+
 template <int NS>
-__global__ void __launch_bounds__(96, VEC_BZ_MINB) vec_burgers_kernel(long E, int Q, const double* __restrict__ coords,
+__global__ void __launch_bounds__(96) vec_burgers_kernel(long E, int Q, const double* __restrict__ coords,
                                                          const double* __restrict__ coef,
                                                          const double* __restrict__ tab, double nu,
                                                          double dt, double* __restrict__ r, int acc) {
-  constexpr int CELLS = 32, NCOEF = 3 * NS, N = 3 * NS;
+  constexpr int CELLS = 16, NCOEF = 3 * NS, N = 3 * NS;
   constexpr int XS = 13, CS = odd(NCOEF), OS = odd(N);
+  constexpr int KA = (NS + 3) / 4, NTJ = (NS + 7) / 8;  // GEMM-A k4 steps; GEMM-C n8 tiles
+  constexpr int VS = 4 * BZQ + 1;                        // V/Y row stride (odd)
+  static_assert(NS % 4 == 0, "u fragments: whole k4 steps");
   __shared__ double sx[CELLS * XS];
   __shared__ double sc[CELLS * (CS > OS ? CS : OS)];
+  __shared__ double sV[3 * CELLS * VS];
+  __shared__ double sK[CELLS * 10];
+  const int Qp = bz_qpad(Q);
   const double* W = tab;
-  const double* Bt = tab + Q;
-  const double* D = Bt + Q * NS;
+  const double* T = tab + Qp;  // [4][Qp][NS]
   const long c0 = (long)blockIdx.x * CELLS;
   const int nt = (int)min((long)CELLS, E - c0);
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t4 = lane & 3;
   stage_rows(sx, XS, coords + c0 * 12, nt, 12);
   stage_rows(sc, CS, coef + c0 * NCOEF, nt, NCOEF);
+  stage_wait();
   __syncthreads();
-  const int cell = threadIdx.x & 31, c = threadIdx.x >> 5;  // c is warp-uniform
-  const double rdt = 1.0 / dt;
-  double rj[NS];
-#pragma unroll
-  for (int j = 0; j < NS; ++j) rj[j] = 0.0;
-  if (cell < nt) {
+  if (tid < CELLS) {
     double x[12];
 #pragma unroll
-    for (int i = 0; i < 12; ++i) x[i] = sx[cell * XS + i];
-    const Geo g = cell_geometry(x);
-    const double* u = sc + cell * CS;
-#pragma unroll 1
-    for (int q = 0; q < Q; ++q) {
-      double uq[3] = {0, 0, 0}, gr[3] = {0, 0, 0};  // u(q); reference gradient of u_c
-#pragma unroll(kBzMUnroll)
-      for (int m = 0; m < NS; ++m) {
-        const double bm = ldro(&Bt[q * NS + m]);
+    for (int i = 0; i < 12; ++i)  // cells past the end: reference tet (never stored)
+      x[i] = tid < nt ? sx[tid * XS + i] : ((i == 3 || i == 7 || i == 11) ? 1.0 : 0.0);
+    const Geo geo = cell_geometry(x);
 #pragma unroll
-        for (int cc = 0; cc < 3; ++cc) uq[cc] = fma(u[cc * NS + m], bm, uq[cc]);
-        const double um = u[c * NS + m];
+    for (int a = 0; a < 3; ++a)
 #pragma unroll
-        for (int a = 0; a < 3; ++a) gr[a] = fma(um, ldro(&D[(a * Q + q) * NS + m]), gr[a]);
-      }
-      double gu[3];  // physical gradient of u_c: gu_b = sum_a K_ab gr_a
+      for (int b = 0; b < 3; ++b) sK[tid * 10 + a * 3 + b] = geo.K[a][b];
+    sK[tid * 10 + 9] = geo.adet;
+  }
+  // GEMM-A A fragments: u_{cell, c, m}, m-tile c, rows g / g+8, k = 4k + t4
+  double ua[3][KA][2];
 #pragma unroll
-      for (int bb = 0; bb < 3; ++bb)
-        gu[bb] = g.K[0][bb] * gr[0] + g.K[1][bb] * gr[1] + g.K[2][bb] * gr[2];
-      const double wq = ldro(&W[q]) * g.adet;
-      const double uc = c == 0 ? uq[0] : (c == 1 ? uq[1] : uq[2]);
-      const double adv = wq * (uc * rdt + uq[0] * gu[0] + uq[1] * gu[1] + uq[2] * gu[2]);
-      double ta[3];  // wq nu sum_b K_ab gu_b
+  for (int c = 0; c < 3; ++c)
 #pragma unroll
-      for (int a = 0; a < 3; ++a)
-        ta[a] = wq * nu * (g.K[a][0] * gu[0] + g.K[a][1] * gu[1] + g.K[a][2] * gu[2]);
-#pragma unroll
-      for (int j = 0; j < NS; ++j)
-        rj[j] = fma(adv, ldro(&Bt[q * NS + j]),
-                    fma(ta[0], ldro(&D[(0 * Q + q) * NS + j]),
-                        fma(ta[1], ldro(&D[(1 * Q + q) * NS + j]),
-                            fma(ta[2], ldro(&D[(2 * Q + q) * NS + j]), rj[j]))));
+    for (int k = 0; k < KA; ++k) {
+      const int m = 4 * k + t4;
+      ua[c][k][0] = g < nt ? sc[g * CS + c * NS + m] : 0.0;
+      ua[c][k][1] = g + 8 < nt ? sc[(g + 8) * CS + c * NS + m] : 0.0;
     }
-  }
-  __syncthreads();  // sc is reused as the output staging
-  if (cell < nt) {
+  double racc[NTJ][4];
 #pragma unroll
-    for (int j = 0; j < NS; ++j) sc[cell * OS + c * NS + j] = rj[j];
+  for (int n = 0; n < NTJ; ++n)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) racc[n][v] = 0.0;
+  const double rdt = 1.0 / dt;
+  __syncthreads();  // sK ready
+#pragma unroll 1
+  for (int q0 = 0; q0 < Qp; q0 += BZQ) {
+    // ---- phase A: warp w -> columns 8w .. 8w+7 = (points q0 + 2w + {0,1}) x (tables 0..3)
+    {
+      double cv[3][4];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) cv[c][v] = 0.0;
+      const int ql = 2 * w + (g >> 2), sb = g & 3;  // this lane's B column (point, table)
+      const double* Tb = T + ((size_t)sb * Qp + q0 + ql) * NS;
+#pragma unroll
+      for (int k = 0; k < KA; ++k) {
+        const double bfr = ldro(&Tb[4 * k + t4]);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) dmma_16x8x4(cv[c], ua[c][k][0], ua[c][k][1], bfr);
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+          sV[(c * CELLS + g + 8 * (v >> 1)) * VS + 8 * w + 2 * t4 + (v & 1)] = cv[c][v];
+    }
+    __syncthreads();
+    // ---- phase B: thread -> (cell, point), in place V -> Y
+    {
+      const int e = tid / BZQ, ql = tid % BZQ;
+      const double* Kc = sK + e * 10;
+      double uq[3], gu[3][3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double* v = sV + (c * CELLS + e) * VS + 4 * ql;
+        uq[c] = v[0];
+#pragma unroll
+        for (int b = 0; b < 3; ++b) gu[c][b] = Kc[0 * 3 + b] * v[1] + Kc[1 * 3 + b] * v[2] + Kc[2 * 3 + b] * v[3];
+      }
+      const double wq = ldro(&W[q0 + ql]) * Kc[9];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        double* y = sV + (c * CELLS + e) * VS + 4 * ql;
+        y[0] = wq * (uq[c] * rdt + uq[0] * gu[c][0] + uq[1] * gu[c][1] + uq[2] * gu[c][2]);
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+          y[1 + a] = wq * nu * (Kc[a * 3 + 0] * gu[c][0] + Kc[a * 3 + 1] * gu[c][1] + Kc[a * 3 + 2] * gu[c][2]);
+      }
+    }
+    __syncthreads();
+    // ---- phase C: warp w = component; k4 step kk = point q0 + kk, k = table t4
+    {
+      const double* y = sV + (w * CELLS) * VS;
+#pragma unroll
+      for (int kk = 0; kk < BZQ; ++kk) {
+        const double a0 = y[g * VS + 4 * kk + t4], a1 = y[(g + 8) * VS + 4 * kk + t4];
+        const double* Tc = T + ((size_t)t4 * Qp + q0 + kk) * NS;
+#pragma unroll
+        for (int n = 0; n < NTJ; ++n) {
+          const int j = 8 * n + g;
+          dmma_16x8x4(racc[n], a0, a1, j < NS ? ldro(&Tc[j]) : 0.0);
+        }
+      }
+    }
+    __syncthreads();  // Y consumed before the next chunk's phase A overwrites it
   }
+  // element vectors: rows g / g+8 = cells, columns j = 8n + 2 t4 (+1), component w
+#pragma unroll
+  for (int n = 0; n < NTJ; ++n)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int cell = g + 8 * (v >> 1), j = 8 * n + 2 * t4 + (v & 1);
+      if (j < NS) sc[cell * OS + w * NS + j] = racc[n][v];
+    }
   __syncthreads();
   store_rows(r + c0 * N, sc, OS, nt, N, acc);
 }
@@ -338,6 +414,8 @@ cudaError_t launch_helm_t(long E, const double* x, const double* f, const double
 }
 
 }  // namespace
+
+int vector_table_qpad(int nq) { return bz_qpad(nq); }
 
 bool vector_supported(int kind, int ns, int nc) {
   switch (kind) {
@@ -381,7 +459,7 @@ cudaError_t launch_vector(int kind, int nq, int ns, int nc, long E, const double
       break;
     case FEMGPU_BURGERS:
       if (ns == 20) {
-        const long grid = (E + 31) / 32;
+        const long grid = (E + 15) / 16;
         vec_burgers_kernel<20><<<(unsigned)grid, 96, 0, s>>>(E, nq, coords, coef, tab, consts[0],
                                                               consts[1], out, acc);
         return cudaGetLastError();
