@@ -147,6 +147,10 @@ __global__ void __launch_bounds__(VEC_THREADS) vec_helm_kernel(long E, const dou
 #ifndef VEC_SVK_MINB
 #define VEC_SVK_MINB 2  // CTAs per SM the SVK residual kernel is register-capped for
 #endif
+#ifndef VEC_SVK_MUNROLL
+#define VEC_SVK_MUNROLL 10  // unroll of its per-point gradient loop over the dofs
+#endif
+constexpr int kSvkMUnroll = VEC_SVK_MUNROLL;
 template <int NS>
 __global__ void __launch_bounds__(VEC_THREADS, VEC_SVK_MINB) vec_svk_kernel(long E, int Q,
                                                               const double* __restrict__ coords,
@@ -191,7 +195,7 @@ __global__ void __launch_bounds__(VEC_THREADS, VEC_SVK_MINB) vec_svk_kernel(long
       }
       // reference gradients of w: gr[c][a] = sum_m w_cm D_a,qm
       double gr[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-#pragma unroll
+#pragma unroll(kSvkMUnroll)
       for (int m = 0; m < NS; ++m) {
         double d[3];
 #pragma unroll
