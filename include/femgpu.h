@@ -144,8 +144,11 @@ int femgpu_assemble_host(const femgpu_form* f, long ncells, const double* coords
  *   o = outputs in name order, t = input tables in name order, c = constants,
  * with femopt's IR naming for this form (paper_1604_05872_b200/ir.py) and
  * HOST pointers.  Per-cell tables are the SoA e-tables (x{v}{c}[e], dofs);
- * reference tables (W, B, D*, P*) are accepted and ignored in favour of the
- * form's own copies.  Outputs are accumulated with `+=` like emitted C.
+ * reference tables (W, B, D*, P*, Dv*, Du*, Dw*) must equal, bit for bit, the
+ * ones the form was created with (its kernels use device copies of those):
+ * FEMGPU_ERR_INCONSISTENT_LAYOUT names the first table that differs.  Burgers
+ * constants (dt, nu) must equal the form's likewise.  Outputs are accumulated
+ * with `+=` like emitted C.
  * `ncells` replaces the literal E of the emitted code. */
 int femgpu_kernel_argv(const femgpu_form* f, long ncells, double* const* o,
                        const double* const* t, const double* c);
@@ -236,8 +239,10 @@ int femgpu_ir_argv(femgpu_ir* k, long ncells, double* const* o, const double* co
 /* The element matrices straight into the global CSR matrix:
  * vals[pos[e][j][k]] += A_e[j][k] (pos from femgpu_csr_positions).  Fused into
  * the element kernel's epilogue where that is faster (P1 Helmholtz: A_e never
- * goes to HBM), else the element kernel into an L2-sized form-owned scratch
- * followed by femgpu_scatter_add.  Device pointers; pos 16-byte aligned. */
+ * goes to HBM), else the element kernel into a form-owned scratch (~256 MiB chunks)
+ * followed by femgpu_scatter_add.  Device pointers; pos 16-byte aligned.
+ * Callers on several streams may share one form: the scratch is handed from
+ * one call's last scatter to the next call's stream by an event. */
 int femgpu_assemble_csr(const femgpu_form* f, long ncells, const double* coords,
                         const double* coeffs, const long* pos, double* vals, void* stream);
 

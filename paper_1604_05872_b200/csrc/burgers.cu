@@ -716,7 +716,8 @@ cudaError_t launch_burgers(int ns, long E, const double* coords, const double* c
              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   const long ntiles = (E + bz::CELLS - 1) / bz::CELLS;
-  const int grid = (int)(ntiles < kNumSMs ? ntiles : kNumSMs);
+  const long nsm = num_sms();
+  const int grid = (int)(ntiles < nsm ? ntiles : nsm);
   burgers_kernel<<<grid, bz::THREADS, bz::SMEM, s>>>(map, E, coords, coef, tab, nu, dt, acc);
   return cudaGetLastError();
 }

@@ -90,6 +90,7 @@ struct femgpu_form {
   std::mutex csr_mu;
   double* csr_scratch = nullptr;
   long csr_chunk = 0;
+  cudaEvent_t csr_done = nullptr;  // recorded after the last scatter that read the scratch
 
   ~femgpu_form() {
     int cur = 0;
@@ -98,6 +99,7 @@ struct femgpu_form {
     if (d_tab) cudaFree(d_tab);
     if (d_vtab) cudaFree(d_vtab);
     if (csr_scratch) cudaFree(csr_scratch);
+    if (csr_done) cudaEventDestroy(csr_done);
     for (int i = 0; i < NSTREAM; ++i) {
       if (host_buf[i]) cudaFree(host_buf[i]);
       if (host_st[i]) cudaStreamDestroy(host_st[i]);
@@ -262,6 +264,53 @@ int coef_column(const femgpu_form* f, const std::string& name) {
       break;
   }
   return -1;
+}
+
+// Values of the reference (non-e) input table `name` as the form's IR defines it
+// (paper_1604_05872_b200/ir.py: W, B, D_a, per-dof P / Du / Dw columns, padded
+// Dv_ca), from the tables the form was created with.  False for e-tables.
+bool expected_table(const femgpu_form* f, const std::string& name, std::vector<double>& v) {
+  const int Q = f->nq, ns = f->ns;
+  auto num = [&](size_t from) { return std::atoi(name.c_str() + from); };
+  auto column = [&](const std::vector<double>& T, size_t off, int ncol, int col) {
+    v.resize(Q);
+    for (int q = 0; q < Q; ++q) v[q] = T[off + (size_t)q * ncol + col];
+  };
+  v.clear();
+  if (name == "W") {
+    v = f->W;
+    return true;
+  }
+  if (name == "B" && (f->kind == FEMGPU_HELMHOLTZ || f->kind == FEMGPU_BURGERS)) {
+    v = f->B;
+    return true;
+  }
+  if (name.size() == 2 && name[0] == 'D' && (f->kind == FEMGPU_HELMHOLTZ || f->kind == FEMGPU_BURGERS)) {
+    const int a = name[1] - '0';
+    v.assign(f->D.begin() + (size_t)a * Q * ns, f->D.begin() + (size_t)(a + 1) * Q * ns);
+    return true;
+  }
+  if (name[0] == 'P') {
+    const int m = num(1);
+    if (f->kind == FEMGPU_BURGERS)
+      column(f->B, 0, ns, m);  // u's basis is the trial space's
+    else
+      column(f->P, 0, f->nc, m);
+    return true;
+  }
+  if (name.size() == 4 && name.rfind("Dv", 0) == 0) {  // component-padded [Q][3 ns]
+    const int c = name[2] - '0', a = name[3] - '0';
+    v.assign((size_t)Q * 3 * ns, 0.0);
+    for (int q = 0; q < Q; ++q)
+      for (int j = 0; j < ns; ++j) v[(size_t)q * 3 * ns + c * ns + j] = Dv(f, a, q, j);
+    return true;
+  }
+  if (name.size() == 5 && (name.rfind("Dw", 0) == 0 || name.rfind("Du", 0) == 0)) {
+    const int a = name[2] - '0', m = num(3);
+    column(f->D, (size_t)a * Q * ns, ns, m);
+    return true;
+  }
+  return false;
 }
 
 void validate(const femgpu_form_desc* d) {
@@ -543,6 +592,9 @@ int femgpu_assemble_host(const femgpu_form* fc, long ncells, const double* coord
     if (ncells < 0) throw Error(FEMGPU_ERR_INVALID_ARG, "negative cell count");
     if (ncells == 0) return;
     if (!coords || !A || (f->ncoef > 0 && !coeffs)) throw Error(FEMGPU_ERR_INVALID_ARG, "null buffer");
+    int cur = 0;  // the form's tables and pipeline buffers live on its device
+    cuda_check(cudaGetDevice(&cur), "cudaGetDevice");
+    if (cur != f->device) throw Error(FEMGPU_ERR_INVALID_ARG, "form belongs to another device");
     std::lock_guard<std::mutex> lock(f->host_mu);
     const size_t nn = (size_t)f->n * f->n;
     // Chunks of at most ~128 MiB of element matrices and at most 1/8 of the
@@ -554,6 +606,7 @@ int femgpu_assemble_host(const femgpu_form* fc, long ncells, const double* coord
     const long chunk = std::min(by_bytes, by_count);
     const size_t per_cell = 12 + f->ncoef + nn;
     if (f->host_chunk != chunk) {
+      f->host_chunk = 0;  // a failed re-allocation leaves no stale size behind
       for (int i = 0; i < femgpu_form::NSTREAM; ++i) {
         if (!f->host_st[i])
           cuda_check(cudaStreamCreateWithFlags(&f->host_st[i], cudaStreamNonBlocking),
@@ -625,10 +678,19 @@ int femgpu_kernel_argv(const femgpu_form* f, long ncells, double* const* o, cons
     if (ncells <= 0) return;
     const long E = ncells;
     const int ns = f->ns;
-    // SoA e-tables -> cell-major (the layout the kernels stream)
+    // SoA e-tables -> cell-major (the layout the kernels stream); reference
+    // tables must equal the form's (its kernels use the form's own copies)
     std::vector<double> coords((size_t)E * 12), coef((size_t)E * std::max(f->ncoef, 1));
+    std::vector<double> want;
     for (size_t i = 0; i < f->argv_tab.size(); ++i) {
       const std::string& name = f->argv_tab[i];
+      if (expected_table(f, name, want)) {
+        if (!t[i]) throw Error(FEMGPU_ERR_INVALID_ARG, "null table " + name);
+        if (std::memcmp(t[i], want.data(), want.size() * sizeof(double)) != 0)
+          throw Error(FEMGPU_ERR_INCONSISTENT_LAYOUT,
+                      "table " + name + " differs from the form's reference tables");
+        continue;
+      }
       if (name.size() == 3 && name[0] == 'x') {
         const int v = name[1] - '0', cc = name[2] - '0';
         if (!t[i]) throw Error(FEMGPU_ERR_INVALID_ARG, "null table " + name);
@@ -727,18 +789,26 @@ int femgpu_assemble_csr(const femgpu_form* fc, long ncells, const double* coords
       return;
     }
     // element kernel into a form-owned scratch, then the scatter-add (chunks of
-    // ~256 MiB, L2-friendly).  A fused copy-out in the warp-specialised tensor
-    // kernels was measured slower: its 4 IO warps cannot issue the atomics of a
-    // 32-cell tile in the time the MMA warps take (c2: 4.5 vs 3.0 ms).
+    // ~256 MiB of element matrices).  A fused copy-out in the warp-specialised
+    // tensor kernels was measured slower: its 4 IO warps cannot issue the atomics
+    // of a 32-cell tile in the time the MMA warps take (c2: 4.5 vs 3.0 ms).
+    // One scratch per form, shared by every caller: the lock orders the enqueues
+    // and the csr_done event orders the GPU work -- this call's stream waits for
+    // the previous call's last scatter (on whatever stream) before overwriting.
     std::lock_guard<std::mutex> lock(f->csr_mu);
     const size_t nn = (size_t)f->n * f->n;
     const long chunk = std::max<long>(64, (long)((256u << 20) / (nn * 8)) / 64 * 64);
+    if (!f->csr_done)
+      cuda_check(cudaEventCreateWithFlags(&f->csr_done, cudaEventDisableTiming), "cudaEventCreate");
     if (!f->csr_scratch || f->csr_chunk != chunk) {
+      cuda_check(cudaEventSynchronize(f->csr_done), "cudaEventSynchronize");
       if (f->csr_scratch) cudaFree(f->csr_scratch);
       f->csr_scratch = nullptr;
+      f->csr_chunk = 0;
       cuda_check(cudaMalloc(&f->csr_scratch, chunk * nn * sizeof(double)), "cudaMalloc(scratch)");
       f->csr_chunk = chunk;
     }
+    cuda_check(cudaStreamWaitEvent(s, f->csr_done, 0), "cudaStreamWaitEvent");
     for (long c0 = 0; c0 < ncells; c0 += chunk) {
       const long E = std::min(chunk, ncells - c0);
       launch(f, E, coords + c0 * 12, f->ncoef > 0 ? coeffs + c0 * f->ncoef : coeffs,
@@ -746,6 +816,7 @@ int femgpu_assemble_csr(const femgpu_form* fc, long ncells, const double* coords
       cuda_check(femgpu::launch_scatter_add(E * (long)nn, f->csr_scratch, pos + c0 * (long)nn, vals, s),
                  "scatter_add_kernel");
     }
+    cuda_check(cudaEventRecord(f->csr_done, s), "cudaEventRecord");
   });
 }
 

@@ -6,7 +6,20 @@
 
 namespace femgpu {
 
-constexpr int kNumSMs = 148;  // B200: 2 dies x 74 SMs
+// SM count of the current device (B200: 148 = 2 dies x 74), queried once per
+// device: persistent grids are sized from it, not from a constant.
+inline int num_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (cache[dev] == 0) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = 148;
+    cache[dev] = n;  // benign race: every writer stores the same value
+  }
+  return cache[dev];
+}
 
 // ---------------------------------------------------------------------------
 // Affine geometry: the level-1 preheader of every femopt IR

@@ -383,7 +383,7 @@ cudaError_t launch_elas_tensor(long E, const double* coords, const double* coef,
   });
   if (e0 != cudaSuccess) return e0;
   const long ntiles = (E + et::CELLS - 1) / et::CELLS;
-  const long maxc = (long)et::CTAS_PER_SM * kNumSMs;
+  const long maxc = (long)et::CTAS_PER_SM * num_sms();
   const int grid = (int)(ntiles < maxc ? ntiles : maxc);
   elas_tensor_kernel<<<grid, et::THREADS, et::SMEM, s>>>(E, coords, coef, tab, A, acc);
   return cudaGetLastError();

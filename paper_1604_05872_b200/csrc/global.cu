@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(256)
 
 int grid_for(long work, int block) {
   const long want = (work + block - 1) / block;
-  const long cap = 8L * kNumSMs * (2048 / block);
+  const long cap = 8L * num_sms() * (2048 / block);
   return (int)(want < cap ? (want > 0 ? want : 1) : cap);
 }
 
@@ -175,7 +175,7 @@ cudaError_t launch_csr_gather_rows(long nrows, int n, int maxlen, const long* ro
   if (wpb < 1) return cudaErrorInvalidValue;
   const size_t smem = rowb * wpb;
   const long want = (nrows + wpb - 1) / wpb;
-  const long cap = 64L * kNumSMs;
+  const long cap = 64L * num_sms();
   const int grid = (int)std::min(want, cap);
   if (n <= 32) {
     auto k = csr_gather_rows_kernel<1>;

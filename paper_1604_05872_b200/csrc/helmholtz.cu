@@ -181,7 +181,7 @@ cudaError_t launch_helm_p1(const HelmP1Params& prm, long E, const double* coords
   });
   if (e0 != cudaSuccess) return e0;
   const long ntiles = (E + P1_TILE - 1) / P1_TILE;
-  const long maxc = (long)P1_CTAS * kNumSMs;
+  const long maxc = (long)P1_CTAS * num_sms();
   const int grid = (int)(ntiles < maxc ? ntiles : maxc);
   if (acc)
     helm_p1_kernel<true><<<grid, P1_TILE, P1_SMEM, s>>>(prm, E, coords, coef, A, pos, vals);
@@ -493,7 +493,7 @@ static cudaError_t launch_tensor_t(long E, const double* coords, const double* c
   });
   if (e0 != cudaSuccess) return e0;
   const long ntiles = (E + Sh::CELLS - 1) / Sh::CELLS;
-  const long max_ctas = kNumSMs;  // persistent: one warp-specialised CTA per SM
+  const long max_ctas = num_sms();  // persistent: one warp-specialised CTA per SM
   const int grid = (int)(ntiles < max_ctas ? ntiles : max_ctas);
   helm_tensor_kernel<NS, NC><<<grid, Sh::THREADS, Sh::SMEM, s>>>(E, coords, coef, Sfrag, A, acc);
   return cudaGetLastError();

@@ -950,7 +950,7 @@ static cudaError_t launch_svk_ws(long E, const double* coords, const double* coe
   });
   if (e0 != cudaSuccess) return e0;
   const long ntiles = (E + Sh::CELLS - 1) / Sh::CELLS;
-  const long maxc = (long)Sh::CTAS_PER_SM * kNumSMs;
+  const long maxc = (long)Sh::CTAS_PER_SM * num_sms();
   const int grid = (int)(ntiles < maxc ? ntiles : maxc);
   kern<<<grid, Sh::THREADS, Sh::SMEM, s>>>(E, coords, coef, tab, A, acc);
   return cudaGetLastError();
@@ -971,7 +971,7 @@ static cudaError_t launch_pair_t(long E, const double* coords, const double* coe
   });
   if (e0 != cudaSuccess) return e0;
   const long ntiles = (E + Sh::CELLS - 1) / Sh::CELLS;
-  const long maxc = (long)Sh::CTAS_PER_SM * kNumSMs;
+  const long maxc = (long)Sh::CTAS_PER_SM * num_sms();
   const int grid = (int)(ntiles < maxc ? ntiles : maxc);
   kern<<<grid, Sh::THREADS, Sh::SMEM, s>>>(E, coords, coef, tab, A, acc);
   return cudaGetLastError();

@@ -122,6 +122,39 @@ def _devptr(x):
     return x.data_ptr()
 
 
+def _invalid(msg: str):
+    raise FemgpuError(9, msg)
+
+
+def _check_dev(t, name: str, rows: int, per_row: int, dtype: str = "float64"):
+    """Validate a device tensor before its pointer reaches native code: CUDA,
+    ``dtype``, C-contiguous, >= ``rows`` rows of ``per_row`` elements.  Raw
+    integer pointers pass through unchecked (the caller vouches for them)."""
+    if t is None or isinstance(t, int):
+        return
+    import torch
+
+    if not isinstance(t, torch.Tensor):
+        _invalid(f"{name}: expected a torch CUDA tensor or a raw device pointer")
+    if not t.is_cuda:
+        _invalid(f"{name}: tensor is not on a CUDA device")
+    if t.dtype != getattr(torch, dtype):
+        _invalid(f"{name}: dtype {t.dtype}, expected torch.{dtype}")
+    if not t.is_contiguous():
+        _invalid(f"{name}: tensor must be C-contiguous")
+    if rows > 0 and (t.dim() == 0 or t.shape[0] < rows or t.numel() < rows * per_row):
+        _invalid(f"{name}: shape {tuple(t.shape)} holds fewer than {rows} x {per_row} elements")
+    if rows > 0 and t.numel() != t.shape[0] * per_row:
+        _invalid(f"{name}: {tuple(t.shape)[1:]} per row, expected {per_row} elements")
+
+
+def _check_host(a, name: str, rows: int, per_row: int):
+    if not isinstance(a, np.ndarray) or a.dtype != np.float64 or not a.flags.c_contiguous:
+        _invalid(f"{name}: expected a C-contiguous float64 numpy array")
+    if a.size < rows * per_row or (rows > 0 and a.size != a.shape[0] * per_row):
+        _invalid(f"{name}: shape {a.shape}, expected [{rows}] x {per_row} elements")
+
+
 class Form:
     """A femgpu form (element-kernel family) bound to the current CUDA device."""
 
@@ -164,11 +197,21 @@ class Form:
         except Exception:
             pass
 
+    def _check_io(self, coords, coeffs, out, E, per_out):
+        if E < 0:
+            return  # the library reports it (FEMGPU_ERR_INVALID_ARG)
+        _check_dev(coords, "coords", E, 12)
+        if self.ncoef > 0:
+            _check_dev(coeffs, "coeffs", E, self.ncoef)
+        if out is not None:
+            _check_dev(out, "out", E, per_out)
+
     # -- device path (the hot path) ------------------------------------------
     def assemble(self, coords, coeffs, out, ncells: int | None = None, accumulate: bool = False,
                  stream=None):
         """Element matrices into ``out`` (device tensors; cell-major layouts)."""
         E = int(coords.shape[0]) if ncells is None else int(ncells)
+        self._check_io(coords, coeffs, out, E, self.n * self.n)
         s = None if stream is None else (stream if isinstance(stream, int) else stream.cuda_stream)
         _check(lib().femgpu_assemble(self.h, E, _devptr(coords), _devptr(coeffs), _devptr(out),
                                      int(accumulate), s))
@@ -178,6 +221,7 @@ class Form:
         """Element vectors [E][n] of the form's family into ``out`` (device tensors):
         Helmholtz load, St Venant--Kirchhoff / Burgers residual (femgpu_assemble_vector)."""
         E = int(coords.shape[0]) if ncells is None else int(ncells)
+        self._check_io(coords, coeffs, out, E, self.n)
         s = None if stream is None else (stream if isinstance(stream, int) else stream.cuda_stream)
         _check(lib().femgpu_assemble_vector(self.h, E, _devptr(coords), _devptr(coeffs),
                                             _devptr(out), int(accumulate), s))
@@ -187,6 +231,9 @@ class Form:
         pos from csr_positions).  Fused into the element kernel where it has a
         CSR epilogue (Helmholtz), else kernel + scatter-add."""
         E = int(coords.shape[0]) if ncells is None else int(ncells)
+        self._check_io(coords, coeffs, None, E, 0)
+        _check_dev(pos, "pos", E, self.n * self.n, "int64")
+        _check_dev(vals, "vals", 0, 1)
         s = None if stream is None else (stream if isinstance(stream, int) else stream.cuda_stream)
         _check(lib().femgpu_assemble_csr(self.h, E, _devptr(coords), _devptr(coeffs),
                                          _devptr(pos), _devptr(vals), s))
@@ -197,8 +244,12 @@ class Form:
         coords = np.ascontiguousarray(coords, dtype=np.float64)
         coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
         E = coords.shape[0]
+        _check_host(coords, "coords", E, 12)
+        if self.ncoef > 0:
+            _check_host(coeffs, "coeffs", E, self.ncoef)
         if out is None:
             out = np.zeros((E, self.n, self.n))
+        _check_host(out, "out", E, self.n * self.n)
         _check(lib().femgpu_assemble_host(self.h, E, _dptr(coords), _dptr(coeffs), _dptr(out),
                                           int(accumulate)))
         return out
@@ -226,11 +277,27 @@ class Form:
 
     def kernel_argv(self, ncells: int, outputs, tables, constants=()):
         """Call like the emitted C: outputs += kernel(tables, constants)."""
-        outs = [np.ascontiguousarray(o) for o in outputs]
-        for o, oo in zip(outs, outputs):
-            if o is not oo:
-                raise ValueError("outputs must be C-contiguous float64 arrays (updated in place)")
+        onames, tnames, cnames = self.argnames()
+        if len(outputs) != len(onames) or len(tables) != len(tnames) or \
+                len(constants) != len(cnames):
+            _invalid(f"kernel_argv takes {len(onames)} outputs, {len(tnames)} tables and "
+                     f"{len(cnames)} constants; got {len(outputs)}, {len(tables)}, "
+                     f"{len(constants)}")
+        per = self.n * self.n // len(onames)  # Burgers: nine (ns x ns) blocks
+        for o, name in zip(outputs, onames):
+            if not isinstance(o, np.ndarray) or o.dtype != np.float64 or \
+                    not o.flags.c_contiguous or not o.flags.writeable:
+                _invalid(f"output {name}: expected a writeable C-contiguous float64 array "
+                         "(updated in place)")
+            if o.size < ncells * per:
+                _invalid(f"output {name}: {o.size} doubles, needs {ncells} x {per}")
+        outs = list(outputs)
         tabs = [np.ascontiguousarray(t, dtype=np.float64) for t in tables]
+        for t, name in zip(tabs, tnames):
+            is_e = name[0] == "x" or name[:1] in ("f", "u", "w") or name[:2] == "mu" or \
+                name[:3] == "lam"
+            if is_e and t.size < ncells:
+                _invalid(f"table {name}: {t.size} values, needs {ncells} (one per cell)")
         cons = np.ascontiguousarray(list(constants) or [0.0], dtype=np.float64)
         dp = C.POINTER(C.c_double)
         op = (dp * len(outs))(*[_dptr(o) for o in outs])

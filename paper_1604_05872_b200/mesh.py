@@ -205,13 +205,25 @@ class GlobalAssembler:
         row-gather assembly (femgpu_csr_gather_rows; bit-reproducible)."""
         from . import femgpu
 
+        import contextlib
+
+        import torch
+
         mode = mode or ("fused" if fused else "scatter")
+        # every step runs on `stream`, the zeroing of the CSR values included
+        # (on torch's current stream it could overlap the atomics)
+        ctx = torch.cuda.stream(stream) if isinstance(stream, torch.cuda.Stream) else \
+            contextlib.nullcontext()
+        if stream is not None and not isinstance(stream, torch.cuda.Stream):
+            raise TypeError("stream must be a torch.cuda.Stream or None")
         self.gather(coef, stream)
         if mode == "fused":
-            self.vals.zero_()
+            with ctx:
+                self.vals.zero_()
             self.form.assemble_csr(self.coords, self.coeffs, self.pos, self.vals, stream=stream)
         elif mode == "scatter":
-            self.vals.zero_()
+            with ctx:
+                self.vals.zero_()
             self.form.assemble(self.coords, self.coeffs, self.A, stream=stream)
             femgpu.scatter_add(self.A, self.pos, self.vals, stream)
         elif mode == "rows":

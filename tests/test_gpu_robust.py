@@ -160,3 +160,109 @@ def test_first_launch_race_fresh_process():
     r = subprocess.run([sys.executable, "-c", _FIRST_LAUNCH_RACE, root], capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+def test_kernel_argv_rejects_foreign_reference_tables():
+    """femgpu_kernel_argv: reference tables that differ from the form's would give
+    results the emitted C would not compute -> INCONSISTENT_LAYOUT (code 8)."""
+    from paper_1604_05872_b200 import ir
+
+    for name in ("c1", "c4", "c5"):
+        cfg = fe.CONFIGS[name]
+        tabs = fe.tables(cfg)
+        form = femgpu.Form.from_config(cfg, tabs)
+        coords, coeffs = fe.cell_inputs(cfg, ncells=5)
+        kernels = ir.build(cfg, coords, coeffs, tabs)
+        tables = {}
+        for _, k in kernels:
+            for tname, t in k["tables"].items():
+                tables[tname] = np.array(t["values"])
+        consts = kernels[0][1].get("constants", {})
+        onames, tnames, cnames = form.argnames()
+        per = form.n * form.n // len(onames)
+        outs = [np.zeros(5 * per) for _ in onames]
+        args = [tables[t] for t in tnames]
+        form.kernel_argv(5, outs, args, [consts[c] for c in cnames])  # the form's own: OK
+        for victim in [t for t in tnames if t[0] in "WBDP"][:3]:
+            bad = [a.copy() for a in args]
+            bad[tnames.index(victim)][0] += 1e-9
+            with pytest.raises(femgpu.FemgpuError) as e:
+                form.kernel_argv(5, outs, bad, [consts[c] for c in cnames])
+            assert e.value.code == 8 and victim in e.value.message
+
+
+def test_python_mirror_validates_buffers():
+    """Wrong dtype / shape / layout / device / argument counts raise
+    FemgpuError(9) before any pointer reaches native code."""
+    cfg = fe.CONFIGS["c2"]
+    form = femgpu.Form.from_config(cfg)
+    dev = torch.device("cuda:0")
+    E = 40
+    coords, coeffs = fe.cell_inputs(cfg, ncells=E)
+    x = torch.from_numpy(coords).to(dev)
+    c = torch.from_numpy(coeffs).to(dev)
+    good = torch.empty((E, cfg.n, cfg.n), dtype=torch.float64, device=dev)
+    form.assemble(x, c, good)
+    bad_outs = [torch.empty((E, cfg.n, cfg.n), dtype=torch.float32, device=dev),
+                torch.empty((E - 1, cfg.n, cfg.n), dtype=torch.float64, device=dev),
+                torch.empty((E, cfg.n, cfg.n + 1), dtype=torch.float64, device=dev),
+                torch.empty((cfg.n, E, cfg.n), dtype=torch.float64, device=dev).transpose(0, 1),
+                torch.empty((E, cfg.n, cfg.n), dtype=torch.float64)]
+    for o in bad_outs:
+        with pytest.raises(femgpu.FemgpuError) as e:
+            form.assemble(x, c, o)
+        assert e.value.code == 9
+    with pytest.raises(femgpu.FemgpuError) as e:
+        form.assemble(x, c[:, :5].contiguous(), good)
+    assert e.value.code == 9
+    with pytest.raises(femgpu.FemgpuError) as e:
+        form.assemble_host(coords, coeffs, np.zeros((E, cfg.n, cfg.n), dtype=np.float32))
+    assert e.value.code == 9
+    onames, tnames, cnames = form.argnames()
+    with pytest.raises(femgpu.FemgpuError) as e:
+        form.kernel_argv(E, [np.zeros(E * cfg.n * cfg.n)], [np.zeros(E)] * (len(tnames) - 1))
+    assert e.value.code == 9
+    with pytest.raises(femgpu.FemgpuError) as e:
+        form.kernel_argv(E, [np.zeros(E * cfg.n * cfg.n, dtype=np.float32)],
+                         [np.zeros(E)] * len(tnames))
+    assert e.value.code == 9
+
+
+def test_assemble_csr_one_form_many_streams():
+    """femgpu_assemble_csr from several threads on distinct streams with ONE form
+    (its element-matrix scratch is shared): every call's CSR values equal the
+    single-stream result up to atomic reordering."""
+    from paper_1604_05872_b200 import mesh
+
+    cfg = fe.CONFIGS["c2"]
+    ga = mesh.GlobalAssembler(cfg, N=6)
+    coef = torch.from_numpy(ga.mesh.global_coeffs()).to(ga.dev)
+    ga.gather(coef)
+    torch.cuda.synchronize()
+    ref = torch.zeros_like(ga.vals)
+    ga.form.assemble_csr(ga.coords, ga.coeffs, ga.pos, ref)
+    torch.cuda.synchronize()
+    results, errors = {}, []
+
+    def run(i):
+        try:
+            s = torch.cuda.Stream(device=ga.dev)
+            with torch.cuda.stream(s):
+                v = torch.zeros_like(ga.vals)
+                for _ in range(4):
+                    v.zero_()
+                    ga.form.assemble_csr(ga.coords, ga.coeffs, ga.pos, v, stream=s)
+            s.synchronize()
+            results[i] = v
+        except Exception as exc:  # noqa: BLE001
+            errors.append(repr(exc))
+
+    threads = [threading.Thread(target=run, args=(i,)) for i in range(6)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    scale = float(ref.abs().max())
+    for v in results.values():
+        assert float((v - ref).abs().max()) <= 1e-13 * scale
