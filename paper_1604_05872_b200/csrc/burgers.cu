@@ -31,9 +31,21 @@
 // the diagonal, and writes the 4x4 block and its mirror into a shared-memory
 // slab [16 cells][20][20].  Warp 15 issues one 3D TMA tensor store per slab
 // (box 20 x 20 x 16 cells, clipped at E; cp.reduce...add for accumulate) and
-// keeps three slabs in flight, so HBM sees long, full-line write streams while
-// the tensor cores work on the next block.  The element matrix (28.8 KB/cell)
-// is written exactly once: this form is HBM-write bound.
+// keeps up to two stores in flight, so HBM sees long, full-line write streams
+// while the tensor cores work on the next block.  The element matrix (28.8 KB
+// per cell) is written exactly once.
+//
+// Tile schedule (BZ_SCHED 1): the six off-diagonal (c,d) blocks need no C, so
+// they go out first, through slabs 1 and 2, with GEMM-2's k4 steps in between
+// (its B fragments stream through a 4-stage ring in slab 0) -- the store stream
+// does not stop while C is built; then the three diagonal blocks (slabs 0, 1, 2).
+// Measured 1.284 vs 1.314 ms (BZ_SCHED 0: GEMM-2 first over an 8-stage ring in
+// slabs 0 and 1, then the nine blocks).  Ablations (BZ_ABL) show the kernel is
+// not HBM-bound: without any TMA store 1.22 ms, without the slab writes 1.01 ms,
+// without GEMM-2 1.13 ms -- the shared-memory crossbar (ring fill and reads,
+// slab writes, the TMA's slab reads) and the DMMA pipe serialise per block.
+// Stores straight from registers (16-byte, full sectors, no staging) ran 2.57 ms:
+// 16 L2 transactions per warp instruction.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -47,8 +59,16 @@
 
 namespace femgpu {
 
+#ifndef BZ_SCHED
+#define BZ_SCHED 1  // 1: GEMM-2 interleaved with the off-diagonal blocks (ring in slab 0);
+                    // 0: GEMM-2 first, then the nine blocks (ring in slabs 0 and 1)
+#endif
+#ifndef BZ_ABL  // development ablations (BZ_SCHED 1): 1 no TMA stores, 2 no GEMM-2,
+                // 4 no GEMM-1 DMMA, 8 no slab writes
+#define BZ_ABL 0
+#endif
 #ifndef BZ_RING_LA
-#define BZ_RING_LA 8  // R2 stages in flight ahead of the consuming k4 step
+#define BZ_RING_LA (BZ_SCHED ? 4 : 8)  // R2 stages in flight ahead of the consuming k4 step
 #endif
 
 namespace bz {
@@ -78,12 +98,12 @@ constexpr int IN_DBL = CELLS * (12 + 3 * NS); // coords | u (bulk-copy target)
 constexpr int CELLD = 10;                     // K(9), adet
 constexpr int NPAIR = 25;                     // GEMM-2 B tile pairs: 15 direct + 10 mirror
 constexpr int STAGE_DBL = NPAIR * 64;         // one k4 step of R2
-constexpr int NRING = 8;                      // ring stages (alias slabs 0 and 1)
+constexpr int NRING = BZ_SCHED ? 4 : 8;        // ring stages (alias slab 0, or slabs 0 and 1)
 constexpr int RING_LA = BZ_RING_LA < NRING ? BZ_RING_LA : NRING;  // stages in flight
 constexpr size_t SMEM =
     sizeof(double) * (size_t)(NSLAB * SLAB_DBL + DN_DBL + 2 * A1_DBL + 2 * A2_DBL + IN_DBL +
                               CELLS * CELLD) + 8 * (1 + 2 * 8 + 2 * 3);
-static_assert(NRING * STAGE_DBL <= 2 * SLAB_DBL, "R2 ring aliases slabs 0 and 1");
+static_assert(NRING * STAGE_DBL <= (BZ_SCHED ? 1 : 2) * SLAB_DBL, "R2 ring aliases slab 0 (and 1)");
 // named barriers (0 = __syncthreads)
 constexpr int BAR_CD = 1;          // compute warps, once per (c,d) block
 constexpr int BAR_FULL = 2;        // + buffer: producer -> compute
@@ -370,6 +390,187 @@ __global__ void __launch_bounds__(bz::THREADS, 1)
   for (int ks = 0; ks < KS1; ++ks)
 #pragma unroll
     for (int h = 0; h < 2; ++h) sb[ks][h] = gS[((ub * KS1 + ks) * 2 + h) * 32 + lane];
+#if BZ_SCHED
+  // GEMM-2 B fragments stream through a ring of k4 stages [25 pairs][32][2]
+  // aliasing slab 0 (BZ_SCHED 1) or slabs 0 and 1 (BZ_SCHED 0)
+  const int pdir = ub, pmir = NBU + bz_off_index(ub);
+  auto ring_issue = [&](long G) {  // stage G = tile * KS2 + ks -> slot G % NRING
+    const int slot = (int)(G % NRING);
+    const int ks = (int)(G % KS2);
+    mbar_expect_tx(&rFull[slot], STAGE_DBL * 8);
+    bulk_g2s(sRing + slot * STAGE_DBL, gR2 + (size_t)ks * STAGE_DBL, STAGE_DBL * 8, &rFull[slot]);
+  };
+  if (issuer && my_tiles > 0 && !(BZ_ABL & 2))
+    for (int ks = 0; ks < RING_LA; ++ks) ring_issue(ks);
+
+  double cdir[2][4], cmir[2][4];
+  // one GEMM-2 k4 step of tile it: C direct (pair pdir) and mirror (pair pmir)
+  auto gemm2_step = [&](long it, int ks, const double* A2, bool refill) {
+    const long G = it * KS2 + ks;
+    const int slot = (int)(G % NRING);
+    mbar_wait(&rFull[slot], (uint32_t)((G / NRING) & 1));
+    BZ_MARK(it, 16, tid == 0 && ks == 0);
+    BZ_MARK(it, 19, tid == 0 && ks == KS2 - 1);
+    const double2* st = reinterpret_cast<const double2*>(sRing + slot * STAGE_DBL);
+    const double2 bd = st[pdir * 32 + lane];
+    const double2 bm = mirror ? st[pmir * 32 + lane] : make_double2(0.0, 0.0);
+    const double2 af = reinterpret_cast<const double2*>(A2)[ks * 32 + lane];
+    __syncwarp();
+    if (lane == 0) mbar_arrive1(&rEmpty[slot]);
+    dmma16x8x4(cdir[0], af.x, af.y, bd.x);
+    dmma16x8x4(cdir[1], af.x, af.y, bd.y);
+    if (mirror) {
+      dmma16x8x4(cmir[0], af.x, af.y, bm.x);
+      dmma16x8x4(cmir[1], af.x, af.y, bm.y);
+    }
+    if (issuer && refill && ks + RING_LA < KS2) {  // stage ks + RING_LA into its slot
+      const long G2 = G + RING_LA;
+      if (G2 >= NRING) mbar_wait(&rEmpty[G2 % NRING], (uint32_t)(((G2 / NRING) - 1) & 1));
+      ring_issue(G2);
+    }
+  };
+
+  // one (c,d) block of tile it: GEMM-1, + C on the diagonal, written into the slab;
+  // the issuer sends the slab with a TMA tensor store once every warp has written it
+  int prev_slab = -1;  // issuer: slab of the previous store in flight
+  // sl: slab, n: its use count (slab 0 once per tile, slabs 1 and 2 four times)
+  auto block = [&](long it, long c0, int cdi, const double* A1, int sl, uint32_t n) {
+    const int c = cdi / 3, d = cdi % 3;
+    double* slab = sSlab + sl * SLAB_DBL;
+    double m[2][4];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) m[h][v] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < KS1; ++ks) {
+      const double2 af = reinterpret_cast<const double2*>(A1)[(cdi * KS1 + ks) * 32 + lane];
+      if (BZ_ABL & 4) {
+        m[0][ks] += af.x * sb[ks][0];
+        m[1][ks] += af.y * sb[ks][1];
+        continue;
+      }
+      dmma16x8x4(m[0], af.x, af.y, sb[ks][0]);
+      dmma16x8x4(m[1], af.x, af.y, sb[ks][1]);
+    }
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {  // odd-g lanes: half 1 first
+      const double m0 = m[0][v], m1 = m[1][v];
+      m[0][v] = hs ? m1 : m0;
+      m[1][v] = hs ? m0 : m1;
+    }
+    double r[2][4];  // mirror values
+#pragma unroll
+    for (int hi = 0; hi < 2; ++hi)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) r[hi][v] = m[hi][v];
+    if (c == d) {
+#pragma unroll
+      for (int hi = 0; hi < 2; ++hi)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          r[hi][v] += cmir[hi][v];
+          m[hi][v] += cdir[hi][v];
+        }
+    }
+    if (n > 0) mbar_wait(&slabEmpty[sl], (n - 1) & 1);
+#pragma unroll
+    for (int hi = 0; hi < 2 && !(BZ_ABL & 8); ++hi) {
+      const int h = hi ^ hs;
+      const int j = 4 * J + 2 * h + (t >> 1);
+      const int k = 4 * K + 2 * (t & 1);
+#pragma unroll
+      for (int vh = 0; vh < 2; ++vh) {
+        double* cellp = slab + (g + 8 * vh) * (NS * NS);
+        *reinterpret_cast<double2*>(cellp + j * NS + k) =
+            make_double2(m[hi][2 * vh], m[hi][2 * vh + 1]);
+        if (mirror) {
+          const bool lo = (t >> 1) == 0;
+          const double other =
+              __shfl_xor_sync(0xffffffffu, lo ? r[hi][2 * vh + 1] : r[hi][2 * vh], 2);
+          const int jj0 = 4 * J + 2 * h;
+          *reinterpret_cast<double2*>(cellp + (k + (lo ? 0 : 1)) * NS + jj0) =
+              lo ? make_double2(r[hi][2 * vh], other) : make_double2(other, r[hi][2 * vh + 1]);
+        }
+      }
+    }
+    fence_proxy_async();  // generic-proxy slab writes -> visible to the TMA unit
+    mbar_arrive1(&slabFull[sl]);
+    if (issuer) {
+      {
+        BZ_T0();
+        mbar_wait(&slabFull[sl], n & 1);
+        BZ_ACC(it, 15);
+      }
+      if (!(BZ_ABL & 1)) slab_store(&amap, slab, d * NS, c * NS, (int)c0, acc);
+      bulk_commit();
+      if (prev_slab >= 0) {
+        BZ_T0();
+        bulk_wait_read1();  // the previous store has left its slab
+        BZ_ACC(it, 18);
+        mbar_arrive1(&slabEmpty[prev_slab]);
+      }
+      prev_slab = sl;
+    }
+  };
+  auto swap_c = [&]() {  // odd-g lanes handle half 1 first: swap C once per tile
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const double d0 = cdir[0][v], d1 = cdir[1][v], m0 = cmir[0][v], m1 = cmir[1][v];
+      cdir[0][v] = hs ? d1 : d0;
+      cdir[1][v] = hs ? d0 : d1;
+      cmir[0][v] = hs ? m1 : m0;
+      cmir[1][v] = hs ? m0 : m1;
+    }
+  };
+
+  // Tile schedule: the six off-diagonal blocks (no C) go out first, through slabs
+  // 1 and 2, with GEMM-2's k4 steps between them -- the TMA store stream never
+  // drains while the tensor cores build C; then the three diagonal blocks (slabs
+  // 0, 1, 2: slab 0 is free once GEMM-2 is done).  Once the first diagonal store
+  // has left slab 0, the issuer refills the ring there for the next tile.
+  for (long it = 0; it < my_tiles; ++it) {
+    const long c0 = (blockIdx.x + it * gridDim.x) * CELLS;
+    const int b = (int)(it & 1);
+    const double* A1 = sA1 + b * A1_DBL;
+    const double* A2 = sA2 + b * A2_DBL;
+    nbar_sync(BAR_FULL + b, THREADS);
+    BZ_MARK(it, 4, tid == 0);
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) cdir[h][v] = cmir[h][v] = 0.0;
+    int ks = 0;
+#pragma unroll 1
+    for (int ob = 0; ob < 6; ++ob) {
+      // off-diagonal (c,d) = 01 02 10 12 20 21 -> cdi 1 2 3 5 6 7
+      block(it, c0, ob + 1 + (ob >= 3), A1, 1 + (ob & 1), (uint32_t)(4 * it + (ob >> 1)));
+      BZ_MARK(it, 6 + ob, tid == 0);
+      const int kend = ((ob + 1) * KS2 + 5) / 6;
+#pragma unroll 1
+      for (; ks < kend && !(BZ_ABL & 2); ++ks) gemm2_step(it, ks, A2, true);
+    }
+    BZ_MARK(it, 5, tid == 0);
+    swap_c();
+    nbar_sync(BAR_CD, CTHREADS);  // every warp's ring reads done before slab 0 is written
+#pragma unroll 1
+    for (int di = 0; di < 3; ++di) {
+      block(it, c0, 4 * di, A1, di, (uint32_t)(di == 0 ? it : 4 * it + 3));
+      BZ_MARK(it, 12 + di, tid == 0);
+      if (issuer && di == 1 && it + 1 < my_tiles && !(BZ_ABL & 2)) {
+        // the first diagonal store (slab 0) has been read (wait_read1 in block):
+        // the next tile's first ring stages into slab 0
+        BZ_MARK(it, 17, true);
+        for (int k = 0; k < RING_LA; ++k) {
+          const long G = (it + 1) * KS2 + k;
+          if (G >= NRING) mbar_wait(&rEmpty[G % NRING], (uint32_t)(((G / NRING) - 1) & 1));
+          ring_issue(G);
+        }
+      }
+    }
+    if (it + 2 < my_tiles) nbar_arrive(BAR_EMPTY + b, THREADS);
+  }
+#else
   // GEMM-2 B fragments stream through a ring of k4 stages [25 pairs][32][2]
   // aliasing slabs 0 and 1 (free while GEMM-2 runs: the last stores of a tile
   // use slabs 2, 1, 0 in that order and have been read by the time we refill)
@@ -527,6 +728,7 @@ __global__ void __launch_bounds__(bz::THREADS, 1)
     }
     if (it + 2 < my_tiles) nbar_arrive(BAR_EMPTY + b, THREADS);
   }
+#endif
   if (issuer) bulk_wait0();
 }
 

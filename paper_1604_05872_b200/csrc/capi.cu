@@ -75,6 +75,7 @@ struct femgpu_form {
   femgpu::HelmP1Params p1{};
   double* d_tab = nullptr;
   size_t tab_doubles = 0;
+  std::vector<double> h_tab;  // host copy of d_tab (kernels that take tables as parameters)
   double* d_vtab = nullptr;  // element-vector tables (femgpu_assemble_vector), if supported
   double flops_per_cell = 0;
   int kernels_per_launch = 1;
@@ -354,7 +355,8 @@ void launch(const femgpu_form* f, long E, const double* coords, const double* co
       e = femgpu::launch_helm_tensor(f->ns, f->nc, E, coords, coef, f->d_tab, A, acc, s);
       break;
     case ROUTE_PAIR:
-      e = femgpu::launch_pair(f->kind, f->nq, f->ns, E, coords, coef, f->d_tab, A, acc, s);
+      e = femgpu::launch_pair(f->kind, f->nq, f->ns, E, coords, coef, f->d_tab, f->h_tab.data(),
+                              A, acc, s);
       break;
     case ROUTE_ELAS_TENSOR:
       e = femgpu::launch_elas_tensor(E, coords, coef, f->d_tab, A, acc, s);
@@ -476,6 +478,7 @@ int femgpu_form_create(const femgpu_form_desc* d, femgpu_form** out) {
     }
     if (!host.empty()) {
       f->tab_doubles = host.size();
+      f->h_tab = host;
       cuda_check(cudaMalloc(&f->d_tab, host.size() * sizeof(double)), "cudaMalloc(tables)");
       cuda_check(cudaMemcpy(f->d_tab, host.data(), host.size() * sizeof(double),
                             cudaMemcpyHostToDevice),

@@ -43,8 +43,8 @@ struct PairParams {
 };
 bool pair_supported(int kind, int nq, int ns);
 cudaError_t launch_pair(int kind, int nq, int ns, long E, const double* coords,
-                        const double* coef, const double* tab, double* A, int acc,
-                        cudaStream_t s);
+                        const double* coef, const double* tab, const double* htab, double* A,
+                        int acc, cudaStream_t s);
 
 // Linear elasticity tensor schedule (see elasticity.cu).
 bool elas_tensor_supported(int ns, int nc);

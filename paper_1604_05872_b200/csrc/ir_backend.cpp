@@ -680,6 +680,18 @@ std::unique_ptr<Kernel> generate(const char* json, int strategy) {
   scan(tree, em);
   for (const auto& o : em.outs)
     if (!em.dims.count(o)) irfail("output " + o + " is never written");
+  // An output without the element index is a sum over the cells (the reference's
+  // corpus kernels, proj/tests/kernels.hpp, accumulate A[j][k] over e): the element
+  // loop is then a reduction, run in order inside one thread like emit_c's loop
+  // (bit-identical), not spread over the grid.
+  if (!em.e_index.empty())
+    for (const auto& o : em.outs) {
+      const auto& dd = em.dims.at(o);
+      if (std::find(dd.begin(), dd.end(), em.e_index) == dd.end()) {
+        em.e_index.clear();
+        break;
+      }
+    }
 
   const bool can_warp = warp_plan(tree, em);
   bool warp = false;

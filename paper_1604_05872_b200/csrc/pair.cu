@@ -42,6 +42,8 @@
 //
 // SVK accumulates each 3x3 (c,d) block as its symmetric and antisymmetric parts
 // (pair_point, svk_unfold): 27 instead of 33 FP64 instructions per pair and point.
+#include <cstring>
+
 #include "common.cuh"
 #include "femgpu_internal.h"
 #include "../../include/femgpu.h"
@@ -75,6 +77,10 @@
 #endif
 #ifndef PAIR_SVK_PW
 #define PAIR_SVK_PW 4  // SVK ws: producer warps
+#endif
+#ifndef PAIR_SVK_PARAMTAB
+#define PAIR_SVK_PARAMTAB 0  // SVK ws: W | D | P as a kernel parameter (constant bank) instead of
+                             // smem (measured: 1.263 vs 1.254 ms on c4, not adopted)
 #endif
 #ifndef PAIR_ABL  // development ablations of pair_ws_kernel: bit 0 no accumulate, bit 1 no store,
                   // bit 2 no records, bit 3 no geometry, bit 4 no staging
@@ -254,7 +260,7 @@ __device__ __forceinline__ void pair_point(double (&a4)[2][2][3][3], double (&t1
 #pragma unroll
     for (int x = 0; x < 2; ++x) {
       double gj[3], ah[3], bh[3], s[3];
-      const double* r = rq + (j0 + x) * JS;
+      const double* r = rq + (j0 + ((PAIR_ABL & 32) ? 0 : x)) * JS;  // 32: timing ablation
 #pragma unroll
       for (int bb = 0; bb < 3; ++bb) {
         gj[bb] = r[bb * CELLS];                // g_j
@@ -327,10 +333,10 @@ __device__ __forceinline__ void svk_unfold(double (&a4)[2][2][3][3]) {
 // E, w'S, mu' F F^T), then the records of the NS basis functions at q: g_j = K^T D phi_j
 // (elasticity), plus h_j = F g_j and s_j = w' S g_j (SVK).  qs / rec: this cell's
 // per-point scalars (stride CELLS) and records (j stride JS, component stride CELLS).
-template <bool SVK, int NS, int Q, int CELLS, int JS, int NCOEF>
+template <bool SVK, int NS, int Q, int CELLS, int JS, int NCOEF, class TW, class TD, class TP>
 __device__ __forceinline__ void pair_point_setup(const double* K, const double* cf, bool valid,
-                                                 int q, const double* sW, const double* sD,
-                                                 const double* sP, double* qs, double* rec) {
+                                                 int q, const TW& sW, const TD& sD, const TP& sP,
+                                                 double* qs, double* rec) {
   auto cv = [&](int r) -> double { return valid ? cf[r] : 0.0; };
   constexpr int CO = SVK ? 3 * NS : 0;  // offset of mu, lam in the dofs
   double muq = 0, lamq = 0;
@@ -749,6 +755,15 @@ __global__ void __launch_bounds__(128, PAIR_FLAT_CTAS)
 }
 
 
+// The reference tables of the SVK ring kernel as a kernel parameter (constant
+// bank c[0]): the producers' table reads leave the shared-memory crossbar.
+template <int NS, int Q>
+struct SvkTables {
+  double W[Q];
+  double D[3 * Q * NS];
+  double P[Q * 4];
+};
+
 // ============================================================================
 // St Venant-Kirchhoff, warp-specialised: NPW producer warps run the per-point setup
 // (one (cell, q) per lane: 32 / CELLS points x CELLS cells per ring stage) into an
@@ -779,7 +794,7 @@ struct SvkWsShape {
   static constexpr int STAGE_DBL = QS * (NS * JS + QSD * CELLS);
   static constexpr int NCOEF = 3 * NS + 8;
   static constexpr int TAB0 = Q + 3 * Q * NS + 4 * Q;
-  static constexpr int TAB = (TAB0 + 1) / 2 * 2;
+  static constexpr int TAB = PAIR_SVK_PARAMTAB ? 0 : (TAB0 + 1) / 2 * 2;
   static constexpr int CELLD = 10;
   static constexpr int IN_DBL = CELLS * (12 + NCOEF);
   static constexpr int CSTRIDE = N * N;                  // one cell per staging buffer
@@ -794,13 +809,14 @@ struct SvkWsShape {
 template <int NS, int Q>
 __global__ void __launch_bounds__(SvkWsShape<NS, Q>::THREADS, SvkWsShape<NS, Q>::CTAS_PER_SM)
     pair_svk_ws_kernel(long E, const double* __restrict__ coords, const double* __restrict__ coef,
-                       const double* __restrict__ tab, double* __restrict__ A, int acc) {
+                       const double* __restrict__ tab, double* __restrict__ A, int acc,
+                       const __grid_constant__ SvkTables<NS, Q> ptab) {
   using Sh = SvkWsShape<NS, Q>;
   constexpr int CELLS = Sh::CELLS, NPW = Sh::NPW, NSLOT = Sh::NSLOT;
   extern __shared__ __align__(16) double smem[];
   double* sW = smem;
   double* sD = sW + Q;                        // [3][Q][NS]
-  double* sP = sD + 3 * Q * NS;               // [Q][4]
+  [[maybe_unused]] double* sP = sD + 3 * Q * NS;  // [Q][4]
   double* sCell = smem + Sh::TAB;             // [2][CELLS][CELLD]          (producers)
   double* sIn = sCell + 2 * CELLS * Sh::CELLD;  // [2][CELLS][12 | NCOEF]   (producers)
   double* sRing = smem + Sh::HEAD;            // [NSLOT][STAGE_DBL]  producers -> consumers
@@ -814,7 +830,8 @@ __global__ void __launch_bounds__(SvkWsShape<NS, Q>::THREADS, SvkWsShape<NS, Q>:
   if ((long)blockIdx.x >= ntiles) return;
   const long my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
 
-  for (int i = tid; i < Sh::TAB0; i += Sh::THREADS) smem[i] = tab[i];
+  if (!PAIR_SVK_PARAMTAB)
+    for (int i = tid; i < Sh::TAB0; i += Sh::THREADS) smem[i] = tab[i];
   if (tid == 0) {
     for (int b = 0; b < NSLOT; ++b) {
       mbar_init(&full[b], 32);
@@ -847,11 +864,11 @@ __global__ void __launch_bounds__(SvkWsShape<NS, Q>::THREADS, SvkWsShape<NS, Q>:
 #pragma unroll
             for (int ql = 0; ql < Sh::QS; ++ql)
               pair_point<Sh>(a4, t1, rec + ql * NS * Sh::JS + sl.cell,
-                             qsb + ql * Sh::QSD * CELLS + sl.cell, sl.j0, sl.k0);
+                            qsb + ql * Sh::QSD * CELLS + sl.cell, sl.j0, sl.k0);
           } else {
             for (int ql = 0; ql < Q - st * Sh::QS; ++ql)
               pair_point<Sh>(a4, t1, rec + ql * NS * Sh::JS + sl.cell,
-                             qsb + ql * Sh::QSD * CELLS + sl.cell, sl.j0, sl.k0);
+                            qsb + ql * Sh::QSD * CELLS + sl.cell, sl.j0, sl.k0);
           }
         }
         __syncwarp();
@@ -926,10 +943,18 @@ __global__ void __launch_bounds__(SvkWsShape<NS, Q>::THREADS, SvkWsShape<NS, Q>:
         if (g >= NSLOT) mbar_wait(&empty[b], (uint32_t)((g / NSLOT - 1) & 1));
         double* rec = sRing + b * Sh::STAGE_DBL;
         const int q = st * Sh::QS + ql;
-        if (q < Q && !(PAIR_ABL & 4))
-          pair_point_setup<true, NS, Q, CELLS, Sh::JS, Sh::NCOEF>(
-              cell + c * Sh::CELLD, in + CELLS * 12 + c * Sh::NCOEF, c < nt, q, sW, sD, sP,
-              rec + Sh::QS * NS * Sh::JS + ql * Sh::QSD * CELLS + c, rec + ql * NS * Sh::JS + c);
+        if (q < Q && !(PAIR_ABL & 4)) {
+          double* qsp = rec + Sh::QS * NS * Sh::JS + ql * Sh::QSD * CELLS + c;
+          double* rp = rec + ql * NS * Sh::JS + c;
+          const double* Kc = cell + c * Sh::CELLD;
+          const double* cf = in + CELLS * 12 + c * Sh::NCOEF;
+          if constexpr (PAIR_SVK_PARAMTAB)
+            pair_point_setup<true, NS, Q, CELLS, Sh::JS, Sh::NCOEF>(Kc, cf, c < nt, q, ptab.W,
+                                                                   ptab.D, ptab.P, qsp, rp);
+          else
+            pair_point_setup<true, NS, Q, CELLS, Sh::JS, Sh::NCOEF>(Kc, cf, c < nt, q, sW, sD, sP,
+                                                                   qsp, rp);
+        }
         mbar_arrive_cta(&full[b]);  // release: this stage's records are visible
       }
     }
@@ -938,8 +963,13 @@ __global__ void __launch_bounds__(SvkWsShape<NS, Q>::THREADS, SvkWsShape<NS, Q>:
 
 template <int NS, int Q>
 static cudaError_t launch_svk_ws(long E, const double* coords, const double* coef,
-                                 const double* tab, double* A, int acc, cudaStream_t s) {
+                                 const double* tab, const double* htab, double* A, int acc,
+                                 cudaStream_t s) {
   using Sh = SvkWsShape<NS, Q>;
+  SvkTables<NS, Q> pt;  // W | D | P, the layout of tab (host copy)
+  static_assert(sizeof(pt) == sizeof(double) * Sh::TAB0, "table layout");
+  if (htab) std::memcpy(&pt, htab, sizeof pt);
+  else if (PAIR_SVK_PARAMTAB) return cudaErrorInvalidValue;
   auto kern = pair_svk_ws_kernel<NS, Q>;
   static const char once_key = 0;  // one per (kernel instantiation, device)
   const cudaError_t e0 = once_per_device(&once_key, [&]() -> cudaError_t {
@@ -952,15 +982,17 @@ static cudaError_t launch_svk_ws(long E, const double* coords, const double* coe
   const long ntiles = (E + Sh::CELLS - 1) / Sh::CELLS;
   const long maxc = (long)Sh::CTAS_PER_SM * num_sms();
   const int grid = (int)(ntiles < maxc ? ntiles : maxc);
-  kern<<<grid, Sh::THREADS, Sh::SMEM, s>>>(E, coords, coef, tab, A, acc);
+  kern<<<grid, Sh::THREADS, Sh::SMEM, s>>>(E, coords, coef, tab, A, acc, pt);
   return cudaGetLastError();
 }
 
 template <int KIND, int NS, int Q>
 static cudaError_t launch_pair_t(long E, const double* coords, const double* coef,
-                                 const double* tab, double* A, int acc, cudaStream_t s) {
+                                 const double* tab, const double* htab, double* A, int acc,
+                                 cudaStream_t s) {
   using Sh = PairShape<KIND, NS, Q>;
-  if constexpr (Sh::SVK && PAIR_SVK_WS) return launch_svk_ws<NS, Q>(E, coords, coef, tab, A, acc, s);
+  if constexpr (Sh::SVK && PAIR_SVK_WS)
+    return launch_svk_ws<NS, Q>(E, coords, coef, tab, htab, A, acc, s);
   auto kern = (Sh::SVK || Sh::FLAT) ? pair_flat_kernel<KIND, NS, Q> : pair_ws_kernel<NS, Q>;
   static const char once_key = 0;  // one per (kernel instantiation, device)
   const cudaError_t e0 = once_per_device(&once_key, [&]() -> cudaError_t {
@@ -985,17 +1017,18 @@ bool pair_supported(int kind, int nq, int ns) {
 }
 
 cudaError_t launch_pair(int kind, int nq, int ns, long E, const double* coords, const double* coef,
-                        const double* tab, double* A, int acc, cudaStream_t s) {
+                        const double* tab, const double* htab, double* A, int acc,
+                        cudaStream_t s) {
   if (E <= 0) return cudaSuccess;
   if (ns == 10) {
     if (kind == FEMGPU_ELASTICITY && nq == 8)
-      return launch_pair_t<FEMGPU_ELASTICITY, 10, 8>(E, coords, coef, tab, A, acc, s);
+      return launch_pair_t<FEMGPU_ELASTICITY, 10, 8>(E, coords, coef, tab, htab, A, acc, s);
     if (kind == FEMGPU_ELASTICITY && nq == 27)
-      return launch_pair_t<FEMGPU_ELASTICITY, 10, 27>(E, coords, coef, tab, A, acc, s);
+      return launch_pair_t<FEMGPU_ELASTICITY, 10, 27>(E, coords, coef, tab, htab, A, acc, s);
     if (kind == FEMGPU_HYPERELASTICITY && nq == 27)
-      return launch_pair_t<FEMGPU_HYPERELASTICITY, 10, 27>(E, coords, coef, tab, A, acc, s);
+      return launch_pair_t<FEMGPU_HYPERELASTICITY, 10, 27>(E, coords, coef, tab, htab, A, acc, s);
     if (kind == FEMGPU_HYPERELASTICITY && nq == 8)
-      return launch_pair_t<FEMGPU_HYPERELASTICITY, 10, 8>(E, coords, coef, tab, A, acc, s);
+      return launch_pair_t<FEMGPU_HYPERELASTICITY, 10, 8>(E, coords, coef, tab, htab, A, acc, s);
   }
   return cudaErrorInvalidValue;
 }
