@@ -232,8 +232,8 @@ def f_alg(cfg_name):
         return None
 
 
-KERNEL_SOURCES = {"helm_": "helmholtz.cu", "pair_": "pair.cu", "burgers": "burgers.cu",
-                  "elas_": "elasticity.cu"}
+KERNEL_SOURCES = {"helm_quad": "helm_quad.cu", "helm_": "helmholtz.cu", "pair_": "pair.cu",
+                  "burgers": "burgers.cu", "elas_": "elasticity.cu"}
 
 
 def kernel_source_sha(kernel_name: str):

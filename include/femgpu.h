@@ -72,7 +72,14 @@ typedef enum femgpu_form_kind {
  *               geometry/coefficient factors (preeval.cpp:279-451)
  *   QUADRATURE  per-quadrature-point sharing-eliminated accumulation
  *               (sharing.cpp:409-607)
- * AUTO picks the schedule this library measured fastest for the form. */
+ * AUTO ranks every kernel this library has for the form by predicted time --
+ * the roofline time max(flops / FP64 peak, bytes / HBM bandwidth) of the
+ * kernel's own flop and byte counts on the current device, divided by the
+ * fraction of that roofline the kernel was measured to reach on B200 -- and
+ * takes the fastest, the GPU counterpart of femopt's theta_pre / theta_se plan
+ * choice (proj/src/cost.cpp:61-116, driver.cpp:47-106).  TENSOR / QUADRATURE
+ * take the best kernel of that schedule.  femgpu_form_schedules() lists the
+ * ranking. */
 typedef enum femgpu_schedule {
   FEMGPU_SCHED_AUTO = 0,
   FEMGPU_SCHED_TENSOR = 1,
@@ -104,6 +111,27 @@ typedef struct femgpu_form_info {
   int kernels_per_launch;     /* device kernels one femgpu_assemble launches */
   char kernel_name[64];       /* dominant kernel's name */
 } femgpu_form_info;
+
+/* One kernel the library could run for a form, with its cost model. */
+typedef struct femgpu_schedule_info {
+  char kernel_name[64];
+  int schedule;                  /* FEMGPU_SCHED_TENSOR or FEMGPU_SCHED_QUADRATURE */
+  int pipe;                      /* FP64 pipe: 0 = DFMA (CUDA cores), 1 = DMMA (tensor) */
+  double flops_per_cell;         /* FP64 flops the kernel executes per cell */
+  double bytes_per_cell;         /* compulsory HBM bytes per cell */
+  double peak_flops;             /* the pipe's FP64 peak on the current device, flop/s */
+  double peak_bytes;             /* HBM bandwidth of the current device, B/s */
+  double efficiency;             /* measured fraction of the roofline (B200, profiles/) */
+  double predicted_ns_per_cell;  /* max(flops/peak_flops, bytes/peak_bytes)/efficiency */
+  int chosen;                    /* 1 for the kernel femgpu_form_create would pick */
+} femgpu_schedule_info;
+
+/* The kernels available for a form descriptor, ranked by predicted time
+ * (fastest first; the one desc->schedule selects has chosen = 1).  Writes at
+ * most cap entries; *count = number available.  Needs a current CUDA device
+ * (its attributes give the peaks); uploads nothing. */
+int femgpu_form_schedules(const femgpu_form_desc* desc, femgpu_schedule_info* out, int cap,
+                          int* count);
 
 /* Creates a form on the current CUDA device: validates the tables, computes
  * the schedule's pre-evaluated reference tensors on the host in FP64

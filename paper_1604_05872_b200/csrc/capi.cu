@@ -57,7 +57,14 @@ int guarded(Fn&& fn) {
   }
 }
 
-enum Route { ROUTE_HELM_P1, ROUTE_HELM_TENSOR, ROUTE_PAIR, ROUTE_ELAS_TENSOR, ROUTE_BURGERS };
+enum Route {
+  ROUTE_HELM_P1,
+  ROUTE_HELM_TENSOR,
+  ROUTE_HELM_QUAD,
+  ROUTE_PAIR,
+  ROUTE_ELAS_TENSOR,
+  ROUTE_BURGERS
+};
 
 std::string two(int m) {
   char b[8];
@@ -138,9 +145,6 @@ void build_helm_p1(femgpu_form* f) {
   }
   for (int j = 0; j < 4; ++j)
     for (int a = 0; a < 3; ++a) p.Dr[j][a] = Dv(f, a, 0, j);
-  // stiffness 10 pairs x (3 mul+2 add) + geometry ~60 + gradients 36*2 + mass/combine
-  f->flops_per_cell = 60 + 72 + 8 + 10 * (5 + 8 + 3);
-  f->kernel_name = "helm_p1_kernel";
 }
 
 void build_helm_tensor(femgpu_form* f, std::vector<double>& host) {
@@ -183,8 +187,6 @@ void build_helm_tensor(femgpu_form* f, std::vector<double>& host) {
           host[((size_t)(ks * NT + nt) * 32 + lane) * 2 + v] =
               (k < KR && n < NP) ? S[(size_t)k * NP + n] : 0.0;
         }
-  f->flops_per_cell = 2.0 * KR * NP + 60 + 36 + KR;
-  f->kernel_name = "helm_tensor_kernel";
 }
 
 void build_argv_names(femgpu_form* f) {
@@ -330,12 +332,138 @@ void validate(const femgpu_form_desc* d) {
     throw Error(FEMGPU_ERR_INVALID_ARG, "unknown schedule");
 }
 
-bool constant_gradients(const femgpu_form* f) {
+bool constant_gradients(const femgpu_form_desc* d) {
   for (int a = 0; a < 3; ++a)
-    for (int q = 1; q < f->nq; ++q)
-      for (int j = 0; j < f->ns; ++j)
-        if (Dv(f, a, q, j) != Dv(f, a, 0, j)) return false;
+    for (int q = 1; q < d->nq; ++q)
+      for (int j = 0; j < d->ns; ++j)
+        if (d->D[((size_t)a * d->nq + q) * d->ns + j] != d->D[((size_t)a * d->nq) * d->ns + j])
+          return false;
   return true;
+}
+
+// ---------------------------------------------------------------------------
+// Schedule choice.  Every kernel that supports a form is a candidate with the
+// FP64 flops it executes and the compulsory bytes it moves per cell; its
+// predicted time is the roofline time on the current device divided by the
+// fraction of the roofline the kernel was measured to reach on B200 at the
+// BASELINE sizes (tools/sched_compare.py -> profiles/schedule_choice_r02.json,
+// nominal peaks from the device attributes).  The reference makes the same
+// choice per monomial from its own flop counts (theta_pre vs theta_se,
+// cost.cpp:61-116; plan search driver.cpp:47-106); on the GPU bytes and the
+// FP64 pipe's rate enter too, so a 5x flop advantage of the tensor schedule
+// (P3 Helmholtz) and an HBM tie between two elasticity schedules are both
+// decided by time.
+// ---------------------------------------------------------------------------
+struct Cand {
+  int route, schedule, pipe;
+  double flops, eff;
+  std::string name;
+};
+
+struct Peaks {
+  double flops, bytes;
+};
+
+Peaks device_peaks() {
+  int dev = 0, sms = 148, clk = 1965000, mclk = 3996000, bus = 8192;
+  if (cudaGetDevice(&dev) == cudaSuccess) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0) sms = v;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrClockRate, dev) == cudaSuccess && v > 0) clk = v;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMemoryClockRate, dev) == cudaSuccess && v > 0) mclk = v;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrGlobalMemoryBusWidth, dev) == cudaSuccess && v > 0) bus = v;
+  }
+  // 64 FP64 FMA lanes per SM per clock (DFMA and DMMA alike on B200); DDR HBM
+  return {(double)sms * clk * 1e3 * 128.0, 2.0 * mclk * 1e3 * bus / 8.0};
+}
+
+// Measured fraction of the nominal roofline per kernel (B200 at 1965 MHz, nominal
+// 37.2 TFLOP/s FP64 and 7.67 TB/s from the device attributes; BASELINE meshes;
+// profiles/schedule_choice_r02.json, tools/sched_compare.py).  The quadrature
+// Helmholtz kernel maps one warp per 4x4 (j,k) tile: ns = 4 keeps one of 16 warps busy.
+constexpr double kEffHelmP1 = 0.831, kEffHelmTensor = 0.754, kEffPairElas = 0.726,
+                 kEffElasTensor = 0.381, kEffPairSvk = 0.432, kEffBurgers = 0.589;
+double eff_helm_quad(int ns) { return ns >= 20 ? 0.245 : ns >= 10 ? 0.2 : 0.04; }
+
+std::vector<Cand> candidates(const femgpu_form_desc* d) {
+  std::vector<Cand> c;
+  const int Q = d->nq, ns = d->ns, nc = d->nc;
+  switch (d->kind) {
+    case FEMGPU_HELMHOLTZ:
+      if (ns == 4 && nc == 4 && constant_gradients(d))
+        // geometry ~60 + gradients 36*2 + mass/combine 8 + stiffness 10 pairs x (5+8+3)
+        c.push_back({ROUTE_HELM_P1, FEMGPU_SCHED_TENSOR, 0, 60 + 72 + 8 + 10 * (5 + 8 + 3.0),
+                     kEffHelmP1, "helm_p1_kernel"});
+      if (femgpu::helm_tensor_supported(ns, nc)) {
+        int KS, NT, KR, NP;
+        femgpu::helm_tensor_geometry(ns, nc, &KS, &NT, &KR, &NP);
+        c.push_back({ROUTE_HELM_TENSOR, FEMGPU_SCHED_TENSOR, 1, 2.0 * KR * NP + 60 + 36 + KR,
+                     kEffHelmTensor, "helm_tensor_kernel"});
+      }
+      if (femgpu::helm_quad_supported(ns, nc)) {
+        // per point: f (2 nc), s (2), records 15 ns, j-side scaling 4 ns, pairs 8 (j<=k)
+        const double per_q = 2.0 * nc + 2 + 15.0 * ns + 4.0 * ns + 8.0 * ns * (ns + 1) / 2;
+        c.push_back({ROUTE_HELM_QUAD, FEMGPU_SCHED_QUADRATURE, 0, 60 + Q * per_q,
+                     eff_helm_quad(ns), "helm_quad_kernel"});
+      }
+      break;
+    case FEMGPU_ELASTICITY:
+      if (femgpu::pair_supported(d->kind, Q, ns))
+        c.push_back({ROUTE_PAIR, FEMGPU_SCHED_QUADRATURE, 0,
+                     60 + Q * (ns * 3 * 5 + 16 + ns * (ns + 1) / 2 * 24.0 * 2), kEffPairElas,
+                     "pair_kernel<elasticity>"});
+      if (femgpu::elas_tensor_supported(ns, nc))
+        // alpha: 6 blocks x 36 x 3; GEMM: 3 full 10x10 + 3 upper halves (55) x 36 x 2
+        c.push_back({ROUTE_ELAS_TENSOR, FEMGPU_SCHED_TENSOR, 1,
+                     60 + 6.0 * 36 * 3 + 2.0 * 36 * (3 * 100 + 3 * 55), kEffElasTensor,
+                     "elas_tensor_kernel"});
+      break;
+    case FEMGPU_HYPERELASTICITY:
+      if (femgpu::pair_supported(d->kind, Q, ns))
+        c.push_back({ROUTE_PAIR, FEMGPU_SCHED_QUADRATURE, 0,
+                     60 + Q * (ns * 3 * 5 + 16 + ns * (ns + 1) / 2 * 33.0 * 2), kEffPairSvk,
+                     "pair_kernel<svk>"});
+      break;
+    case FEMGPU_BURGERS:
+      if (femgpu::burgers_supported(Q, ns)) {
+        const double r = 10;  // derivative-space rank of P3 (checked when the tables are built)
+        // g^{cd}: 3c x 3a x r x 20 + 9 x r x 3; GEMM-1: 9 (c,d) x r x 210 (j<=k);
+        // GEMM-2: 67 x 400; geometry + GEMM-2 A
+        c.push_back({ROUTE_BURGERS, FEMGPU_SCHED_TENSOR, 1,
+                     2.0 * 9 * r * 20 + 2.0 * 9 * r * 3 + 2.0 * 9 * r * 210 + 2.0 * 67 * 400 +
+                         60 * 7 + 60,
+                     kEffBurgers, "burgers_kernel"});
+      }
+      break;
+  }
+  return c;
+}
+
+double bytes_per_cell(const femgpu_form_desc* d) {
+  const int n = d->kind == FEMGPU_HELMHOLTZ ? d->ns : 3 * d->ns;
+  const int ncoef = d->kind == FEMGPU_HELMHOLTZ       ? d->nc
+                    : d->kind == FEMGPU_ELASTICITY      ? 8
+                    : d->kind == FEMGPU_HYPERELASTICITY ? 3 * d->ns + 8
+                                                       : 3 * d->ns;
+  return 8.0 * (12 + ncoef + (double)n * n);
+}
+
+double predicted_ns(const Cand& c, double bytes, const Peaks& pk) {
+  return std::max(c.flops / pk.flops, bytes / pk.bytes) / c.eff * 1e9;
+}
+
+// Candidates ranked by predicted time; index of the one `schedule` selects, or -1.
+int rank_schedules(const femgpu_form_desc* d, std::vector<Cand>& c) {
+  c = candidates(d);
+  const Peaks pk = device_peaks();
+  const double b = bytes_per_cell(d);
+  std::stable_sort(c.begin(), c.end(), [&](const Cand& x, const Cand& y) {
+    const double tx = predicted_ns(x, b, pk), ty = predicted_ns(y, b, pk);
+    return tx != ty ? tx < ty : x.flops < y.flops;
+  });
+  for (size_t i = 0; i < c.size(); ++i)
+    if (d->schedule == FEMGPU_SCHED_AUTO || d->schedule == c[i].schedule) return (int)i;
+  return -1;
 }
 
 void check_ptr(const void* p, const char* what) {
@@ -353,6 +481,9 @@ void launch(const femgpu_form* f, long E, const double* coords, const double* co
       break;
     case ROUTE_HELM_TENSOR:
       e = femgpu::launch_helm_tensor(f->ns, f->nc, E, coords, coef, f->d_tab, A, acc, s);
+      break;
+    case ROUTE_HELM_QUAD:
+      e = femgpu::launch_helm_quad(f->ns, f->nq, f->nc, E, coords, coef, f->d_tab, A, acc, s);
       break;
     case ROUTE_PAIR:
       e = femgpu::launch_pair(f->kind, f->nq, f->ns, E, coords, coef, f->d_tab, f->h_tab.data(),
@@ -415,66 +546,45 @@ int femgpu_form_create(const femgpu_form_desc* d, femgpu_form** out) {
     if (d->nc > 0) f->P.assign(d->P, d->P + (size_t)d->nq * d->nc);
     cuda_check(cudaGetDevice(&f->device), "cudaGetDevice");
     std::vector<double> host;
-    switch (d->kind) {
-      case FEMGPU_HELMHOLTZ:
-        if (d->ns == 4 && d->nc == 4 && constant_gradients(f.get()) &&
-            d->schedule != FEMGPU_SCHED_QUADRATURE) {
-          f->route = ROUTE_HELM_P1;
-          build_helm_p1(f.get());
-        } else if (femgpu::helm_tensor_supported(d->ns, d->nc) &&
-                   d->schedule != FEMGPU_SCHED_QUADRATURE) {
-          f->route = ROUTE_HELM_TENSOR;
-          build_helm_tensor(f.get(), host);
-        } else {
-          throw Error(FEMGPU_ERR_UNSUPPORTED, "no Helmholtz kernel for ns=" +
-                                                  std::to_string(d->ns) + " nc=" + std::to_string(d->nc));
-        }
-        f->schedule = FEMGPU_SCHED_TENSOR;
+    std::vector<Cand> cands;
+    const int pick = rank_schedules(d, cands);
+    if (pick < 0)
+      throw Error(FEMGPU_ERR_UNSUPPORTED,
+                  cands.empty() ? "no kernel for this form's sizes"
+                                : "no kernel of the requested schedule for this form");
+    const Cand& ch = cands[pick];
+    f->route = ch.route;
+    f->schedule = ch.schedule;
+    f->flops_per_cell = ch.flops;
+    f->kernel_name = ch.name;
+    switch (ch.route) {
+      case ROUTE_HELM_P1:
+        build_helm_p1(f.get());
         break;
-      case FEMGPU_ELASTICITY:
-        if (femgpu::elas_tensor_supported(d->ns, d->nc) && d->schedule == FEMGPU_SCHED_TENSOR) {
-          f->route = ROUTE_ELAS_TENSOR;
-          f->schedule = FEMGPU_SCHED_TENSOR;
-          host.assign(femgpu::elas_tensor_table_doubles(), 0.0);
-          femgpu::elas_tensor_tables(f->nq, f->W.data(), f->D.data(), f->P.data(), host.data());
-          // alpha: 6 blocks x 36 x 3; GEMM: 3 full 10x10 + 3 upper halves (55) x 36 x 2
-          f->flops_per_cell = 60 + 6.0 * 36 * 3 + 2.0 * 36 * (3 * 100 + 3 * 55);
-          f->kernel_name = "elas_tensor_kernel";
-          break;
-        }
-        [[fallthrough]];
-      case FEMGPU_HYPERELASTICITY: {
-        if (!femgpu::pair_supported(d->kind, d->nq, d->ns) || d->schedule == FEMGPU_SCHED_TENSOR)
-          throw Error(FEMGPU_ERR_UNSUPPORTED, "no vector-form kernel for this size/schedule");
-        f->route = ROUTE_PAIR;
-        f->schedule = FEMGPU_SCHED_QUADRATURE;
+      case ROUTE_HELM_TENSOR:
+        build_helm_tensor(f.get(), host);
+        break;
+      case ROUTE_HELM_QUAD:  // W | B | D | P
+        host.insert(host.end(), f->W.begin(), f->W.end());
+        host.insert(host.end(), f->B.begin(), f->B.end());
+        host.insert(host.end(), f->D.begin(), f->D.end());
+        host.insert(host.end(), f->P.begin(), f->P.end());
+        break;
+      case ROUTE_ELAS_TENSOR:
+        host.assign(femgpu::elas_tensor_table_doubles(), 0.0);
+        femgpu::elas_tensor_tables(f->nq, f->W.data(), f->D.data(), f->P.data(), host.data());
+        break;
+      case ROUTE_PAIR:  // W | D | P
         host.insert(host.end(), f->W.begin(), f->W.end());
         host.insert(host.end(), f->D.begin(), f->D.end());
         host.insert(host.end(), f->P.begin(), f->P.end());
-        const int npair = f->ns * (f->ns + 1) / 2;
-        const double per_q = d->kind == FEMGPU_ELASTICITY ? 24.0 : 33.0;  // SVK: symmetric/antisymmetric split
-        f->flops_per_cell = 60 + f->nq * (f->ns * 3 * 5 + 16 + npair * per_q * 2);
-        f->kernel_name = d->kind == FEMGPU_ELASTICITY ? "pair_kernel<elasticity>" : "pair_kernel<svk>";
         break;
-      }
-      case FEMGPU_BURGERS:
-        if (!femgpu::burgers_supported(d->nq, d->ns) || d->schedule == FEMGPU_SCHED_QUADRATURE)
-          throw Error(FEMGPU_ERR_UNSUPPORTED, "no Burgers kernel for this size/schedule");
-        f->route = ROUTE_BURGERS;
-        f->schedule = FEMGPU_SCHED_TENSOR;
+      case ROUTE_BURGERS:
         host.assign(femgpu::burgers_table_doubles(), 0.0);
-        {
-          const int r = femgpu::burgers_tables(f->nq, f->W.data(), f->B.data(), f->D.data(),
-                                               host.data());
-          if (r < 0)
-            throw Error(FEMGPU_ERR_UNSUPPORTED,
-                        "Burgers kernel: derivative tables do not span a space of rank <= 12");
-          // g^{cd}: 3c x 3a x r x 20 + 9 x r x 3; GEMM-1: 9 (c,d) x r x 210 (j<=k);
-          // GEMM-2: 67 x 400; geometry + GEMM-2 A
-          f->flops_per_cell = 2.0 * 9 * r * 20 + 2.0 * 9 * r * 3 + 2.0 * 9 * r * 210 +
-                              2.0 * 67 * 400 + 60 * 7 + 60;
-        }
-        f->kernel_name = "burgers_kernel";
+        if (femgpu::burgers_tables(f->nq, f->W.data(), f->B.data(), f->D.data(), host.data()) < 0)
+          throw Error(FEMGPU_ERR_UNSUPPORTED,
+                      "Burgers kernel: derivative tables do not span a space of rank <= 12");
+        break;
     }
     if (!host.empty()) {
       f->tab_doubles = host.size();
@@ -524,6 +634,36 @@ int femgpu_form_create(const femgpu_form_desc* d, femgpu_form** out) {
 }
 
 void femgpu_form_free(femgpu_form* f) { delete f; }
+
+int femgpu_form_schedules(const femgpu_form_desc* d, femgpu_schedule_info* out, int cap,
+                          int* count) {
+  if (!count || (cap > 0 && !out)) {
+    g_last_error = "null argument";
+    return FEMGPU_ERR_INVALID_ARG;
+  }
+  return guarded([&] {
+    validate(d);
+    std::vector<Cand> c;
+    const int pick = rank_schedules(d, c);
+    const Peaks pk = device_peaks();
+    const double b = bytes_per_cell(d);
+    *count = (int)c.size();
+    for (int i = 0; i < (int)c.size() && i < cap; ++i) {
+      femgpu_schedule_info& o = out[i];
+      std::memset(&o, 0, sizeof o);
+      std::snprintf(o.kernel_name, sizeof o.kernel_name, "%s", c[i].name.c_str());
+      o.schedule = c[i].schedule;
+      o.pipe = c[i].pipe;
+      o.flops_per_cell = c[i].flops;
+      o.bytes_per_cell = b;
+      o.peak_flops = pk.flops;
+      o.peak_bytes = pk.bytes;
+      o.efficiency = c[i].eff;
+      o.predicted_ns_per_cell = predicted_ns(c[i], b, pk);
+      o.chosen = i == pick;
+    }
+  });
+}
 
 int femgpu_form_get_info(const femgpu_form* f, femgpu_form_info* info) {
   if (!f || !info) {

@@ -35,6 +35,12 @@ void helm_tensor_geometry(int ns, int nc, int* KS, int* NT, int* KR, int* NP);
 cudaError_t launch_helm_tensor(int ns, int nc, long E, const double* coords, const double* coef,
                                const double* Sfrag, double* A, int acc, cudaStream_t s);
 
+// Helmholtz in the quadrature schedule (helm_quad.cu); tab = [W | B | D | P].
+bool helm_quad_supported(int ns, int nc);
+cudaError_t launch_helm_quad(int ns, int nq, int nc, long E, const double* coords,
+                             const double* coef, const double* tab, double* A, int acc,
+                             cudaStream_t s);
+
 // Vector forms on CUDA cores: per-(j<=k) pair accumulation over quadrature
 // points (elasticity, St Venant-Kirchhoff).  tab = [W(Q) | D(3,Q,ns) | P(Q,4)].
 struct PairParams {

@@ -38,7 +38,8 @@ ERROR_NAMES = {
 }
 
 # Every symbol include/femgpu.h declares (checked by tests/test_abi.py).
-EXPORTS = ("femgpu_form_create", "femgpu_form_free", "femgpu_form_get_info", "femgpu_assemble",
+EXPORTS = ("femgpu_form_create", "femgpu_form_free", "femgpu_form_get_info",
+           "femgpu_form_schedules", "femgpu_assemble",
            "femgpu_assemble_vector",
            "femgpu_assemble_host", "femgpu_kernel_argv", "femgpu_kernel_argc",
            "femgpu_kernel_argname", "femgpu_gather", "femgpu_csr_positions",
@@ -63,6 +64,14 @@ class FormDesc(C.Structure):
                 ("consts", C.c_double * 4), ("schedule", C.c_int)]
 
 
+class ScheduleInfo(C.Structure):
+    _fields_ = [("kernel_name", C.c_char * 64), ("schedule", C.c_int), ("pipe", C.c_int),
+                ("flops_per_cell", C.c_double), ("bytes_per_cell", C.c_double),
+                ("peak_flops", C.c_double), ("peak_bytes", C.c_double),
+                ("efficiency", C.c_double), ("predicted_ns_per_cell", C.c_double),
+                ("chosen", C.c_int)]
+
+
 class FormInfo(C.Structure):
     _fields_ = [("n", C.c_int), ("ncoef", C.c_int), ("schedule", C.c_int),
                 ("flops_per_cell", C.c_double), ("bytes_per_cell", C.c_double),
@@ -85,6 +94,8 @@ def lib():
         L.femgpu_form_free.argtypes = [vp]
         L.femgpu_form_free.restype = None
         L.femgpu_form_get_info.argtypes = [vp, C.POINTER(FormInfo)]
+        L.femgpu_form_schedules.argtypes = [C.POINTER(FormDesc), C.POINTER(ScheduleInfo), C.c_int,
+                                            C.POINTER(C.c_int)]
         L.femgpu_assemble.argtypes = [vp, C.c_long, vp, vp, vp, C.c_int, vp]
         L.femgpu_assemble_vector.argtypes = [vp, C.c_long, vp, vp, vp, C.c_int, vp]
         L.femgpu_assemble_host.argtypes = [vp, C.c_long, dp, dp, dp, C.c_int]
@@ -155,22 +166,48 @@ def _check_host(a, name: str, rows: int, per_row: int):
         _invalid(f"{name}: shape {a.shape}, expected [{rows}] x {per_row} elements")
 
 
+def _desc(kind: int, tables: "fe.Tables", consts=(), schedule: int = SCHED_AUTO):
+    """A femgpu_form_desc over (kept-alive) contiguous copies of the tables."""
+    keep = [np.ascontiguousarray(tables.W, dtype=np.float64),
+            np.ascontiguousarray(tables.B, dtype=np.float64),
+            np.ascontiguousarray(tables.D, dtype=np.float64),
+            np.ascontiguousarray(tables.P, dtype=np.float64)]
+    W, B, D, P = keep
+    d = FormDesc()
+    d.kind, d.nq, d.ns, d.nc = kind, W.shape[0], B.shape[1], P.shape[1]
+    d.W, d.B, d.D, d.P = _dptr(W), _dptr(B), _dptr(D), _dptr(P)
+    cs = list(consts) + [0.0] * (4 - len(consts))
+    d.consts = (C.c_double * 4)(*cs)
+    d.schedule = schedule
+    return d, keep
+
+
+def schedules(cfg: "fe.Config", tables: "fe.Tables | None" = None,
+              schedule: int = SCHED_AUTO) -> list[dict]:
+    """The kernels available for a config's form, ranked by the library's cost model
+    (femgpu_form_schedules: roofline time on the current device / measured efficiency,
+    fastest first; ``chosen`` marks the one ``schedule`` selects)."""
+    d, _keep = _desc(cfg.kind, tables or fe.tables(cfg), cfg.consts, schedule)
+    out = (ScheduleInfo * 8)()
+    n = C.c_int()
+    _check(lib().femgpu_form_schedules(C.byref(d), out, 8, C.byref(n)))
+    res = []
+    for i in range(min(n.value, 8)):
+        o = out[i]
+        res.append({"kernel": o.kernel_name.decode(), "schedule": SCHEDULE_NAMES[o.schedule],
+                    "pipe": "DMMA" if o.pipe else "DFMA", "flops_per_cell": o.flops_per_cell,
+                    "bytes_per_cell": o.bytes_per_cell, "peak_flops": o.peak_flops,
+                    "peak_bytes": o.peak_bytes, "efficiency": o.efficiency,
+                    "predicted_ns_per_cell": o.predicted_ns_per_cell, "chosen": bool(o.chosen)})
+    return res
+
+
 class Form:
     """A femgpu form (element-kernel family) bound to the current CUDA device."""
 
     def __init__(self, kind: int, tables: "fe.Tables", consts=(), schedule: int = SCHED_AUTO):
         self.kind = kind
-        self._keep = [np.ascontiguousarray(tables.W, dtype=np.float64),
-                      np.ascontiguousarray(tables.B, dtype=np.float64),
-                      np.ascontiguousarray(tables.D, dtype=np.float64),
-                      np.ascontiguousarray(tables.P, dtype=np.float64)]
-        W, B, D, P = self._keep
-        d = FormDesc()
-        d.kind, d.nq, d.ns, d.nc = kind, W.shape[0], B.shape[1], P.shape[1]
-        d.W, d.B, d.D, d.P = _dptr(W), _dptr(B), _dptr(D), _dptr(P)
-        cs = list(consts) + [0.0] * (4 - len(consts))
-        d.consts = (C.c_double * 4)(*cs)
-        d.schedule = schedule
+        d, self._keep = _desc(kind, tables, consts, schedule)
         self.h = C.c_void_p()
         _check(lib().femgpu_form_create(C.byref(d), C.byref(self.h)))
         inf = FormInfo()
