@@ -63,6 +63,9 @@ namespace femgpu {
 #define BZ_SCHED 1  // 1: GEMM-2 interleaved with the off-diagonal blocks (ring in slab 0);
                     // 0: GEMM-2 first, then the nine blocks (ring in slabs 0 and 1)
 #endif
+#ifndef BZ_KFRONT
+#define BZ_KFRONT 0  // BZ_SCHED 1: extra GEMM-2 k4 steps after the first off-diagonal block
+#endif
 #ifndef BZ_ABL  // development ablations (BZ_SCHED 1): 1 no TMA stores, 2 no GEMM-2,
                 // 4 no GEMM-1 DMMA, 8 no slab writes
 #define BZ_ABL 0
@@ -546,7 +549,9 @@ __global__ void __launch_bounds__(bz::THREADS, 1)
       // off-diagonal (c,d) = 01 02 10 12 20 21 -> cdi 1 2 3 5 6 7
       block(it, c0, ob + 1 + (ob >= 3), A1, 1 + (ob & 1), (uint32_t)(4 * it + (ob >> 1)));
       BZ_MARK(it, 6 + ob, tid == 0);
-      const int kend = ((ob + 1) * KS2 + 5) / 6;
+      // GEMM-2 k4 steps done by the end of this block's chunk: BZ_KFRONT steps with
+      // the first block, the rest spread evenly over the six
+      const int kend = BZ_KFRONT + ((ob + 1) * (KS2 - BZ_KFRONT) + 5) / 6;
 #pragma unroll 1
       for (; ks < kend && !(BZ_ABL & 2); ++ks) gemm2_step(it, ks, A2, true);
     }

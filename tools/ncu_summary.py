@@ -64,6 +64,16 @@ def summarise(path):
     return res
 
 
+def src_sha(kernel_name):
+    """sha of the kernel's .cu source (bench.py KERNEL_SOURCES): bench.py uses a
+    capture only while the source it was taken from is unchanged."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    base = (kernel_name or "").split("(")[0].replace("void ", "").replace("femgpu::", "")
+    return bench.kernel_source_sha(base)
+
+
 def main():
     tag = sys.argv[1]
     dst = os.path.join(ROOT, "profiles", "ncu_summary.json")
@@ -76,6 +86,7 @@ def main():
         cfg, path = arg.split("=", 1)
         r = summarise(path)
         r["capture"] = f"{tag}: ncu --set full --clock-control none (1 launch, cold)"
+        r["src_sha"] = src_sha(r.get("kernel"))
         allres.setdefault(cfg, {}).update(r)  # keep other tools' fields (ncu_flops.py)
         print(cfg, json.dumps(r))
     with open(dst, "w") as f:
