@@ -411,7 +411,7 @@ std::vector<Cand> candidates(const femgpu_form_desc* d) {
       if (femgpu::pair_supported(d->kind, Q, ns))
         c.push_back({ROUTE_PAIR, FEMGPU_SCHED_QUADRATURE, 0,
                      60 + Q * (ns * 3 * 5 + 16 + ns * (ns + 1) / 2 * 24.0 * 2), kEffPairElas,
-                     "pair_kernel<elasticity>"});
+                     "pair_ws_kernel"});
       if (femgpu::elas_tensor_supported(ns, nc))
         // alpha: 6 blocks x 36 x 3; GEMM: 3 full 10x10 + 3 upper halves (55) x 36 x 2
         c.push_back({ROUTE_ELAS_TENSOR, FEMGPU_SCHED_TENSOR, 1,
@@ -422,7 +422,7 @@ std::vector<Cand> candidates(const femgpu_form_desc* d) {
       if (femgpu::pair_supported(d->kind, Q, ns))
         c.push_back({ROUTE_PAIR, FEMGPU_SCHED_QUADRATURE, 0,
                      60 + Q * (ns * 3 * 5 + 16 + ns * (ns + 1) / 2 * 33.0 * 2), kEffPairSvk,
-                     "pair_kernel<svk>"});
+                     "pair_svk_ws_kernel"});
       break;
     case FEMGPU_BURGERS:
       if (femgpu::burgers_supported(Q, ns)) {

@@ -17,8 +17,8 @@ import pytest
 from paper_1604_05872_b200 import fe, femgpu
 
 TOL = 1e-12
-EXPECT = {"c1": "helm_p1_kernel", "c2": "helm_tensor_kernel", "c3": "pair_kernel<elasticity>",
-          "c4": "pair_kernel<svk>", "c5": "burgers_kernel"}
+EXPECT = {"c1": "helm_p1_kernel", "c2": "helm_tensor_kernel", "c3": "pair_ws_kernel",
+          "c4": "pair_svk_ws_kernel", "c5": "burgers_kernel"}
 
 
 @pytest.mark.parametrize("name", sorted(EXPECT))
