@@ -232,17 +232,29 @@ int femgpu_csr_gather_rows(long nrows, int n, const long* row_ptr, const long* i
  * kernel IR JSON (proj/README.md:68-100, raw or as femopt_kernel_to_json writes
  * it), generates CUDA for it and compiles it with NVRTC for sm_100a.  Argument
  * groups and order are emit_c's: outputs, input tables, constants, each sorted
- * by name (emit_c.cpp:137-140); outputs are accumulated with +=; results are
- * bit-identical to femopt's emitted C compiled with -ffp-contract=off.
+ * by name (emit_c.cpp:137-140); outputs are accumulated with +=.  The thread
+ * and warp mappings are bit-identical to femopt's emitted C compiled with
+ * -ffp-contract=off.  The GEMM mapping applies to femopt's pre-evaluated
+ * (tensor) plans -- an element body of scalar statements followed by one nest
+ * OUT[e][j][k] += sum_t T_t[j][k] * p_t with T_t pre-evaluated tables and p_t
+ * products of scalars (preeval.cpp:279-451): a generated kernel evaluates the
+ * p_t per cell and a DMMA GEMM contracts them with the tables (different
+ * summation order: within rounding of the emitted C, not bit-identical).  AUTO
+ * takes it when the nest has >= 2048 multiply-adds per cell.
  * ------------------------------------------------------------------------- */
 typedef struct femgpu_ir femgpu_ir;
 
-enum { FEMGPU_IR_AUTO = 0, FEMGPU_IR_THREAD_PER_CELL = 1, FEMGPU_IR_WARP_PER_CELL = 2 };
+enum {
+  FEMGPU_IR_AUTO = 0,
+  FEMGPU_IR_THREAD_PER_CELL = 1,
+  FEMGPU_IR_WARP_PER_CELL = 2,
+  FEMGPU_IR_GEMM = 3
+};
 
 typedef struct {
   int noutputs, ninputs, nconstants;
   int per_cell;  /* 1: the nest has an order-free element loop (ncells applies) */
-  int strategy;  /* FEMGPU_IR_THREAD_PER_CELL or FEMGPU_IR_WARP_PER_CELL */
+  int strategy;  /* FEMGPU_IR_THREAD_PER_CELL, FEMGPU_IR_WARP_PER_CELL or FEMGPU_IR_GEMM */
 } femgpu_ir_info;
 
 /* Parse, generate and compile (FEMGPU_ERR_NOT_FEM_NEST for an IR it cannot

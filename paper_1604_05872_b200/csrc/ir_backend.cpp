@@ -489,6 +489,18 @@ struct Kernel {
   std::map<std::string, long> ext;
   std::string e_index;
   bool warp = false;
+  // GEMM mapping (femopt's pre-evaluated nests): the generated kernel writes
+  // P[e][t] (ldp = Kp), then C[e][n] += P[e][:] . Bm[:][n] on DMMA
+  bool gemm = false;
+  int gK = 0, gKp = 0, gN = 0, gldb = 0;
+  std::vector<double> gB;                    // [Kp][ldb], zero-padded
+  std::map<int, double*> gB_dev;             // per device
+  struct Scratch {
+    double* p = nullptr;
+    size_t n = 0;
+    cudaEvent_t done = nullptr;  // recorded after the last GEMM that read it
+  };
+  std::map<int, Scratch> gP_dev;             // P buffer per device, reused across launches
   std::vector<char> cubin;
   cudaLibrary_t lib = nullptr;
   cudaKernel_t kern = nullptr;
@@ -627,6 +639,98 @@ void plan_distribution(const std::vector<Node>& body, Emitter& em) {
   }
 }
 
+// femopt's pre-evaluated (tensor) nest as a GEMM (preeval.cpp:279-451): the element
+// body is scalar statements then ONE nest j { k { OUT[e][j][k] += sum_t T_t[j][k] * p_t } }
+// with T_t pre-evaluated [j][k] (or [k][j]) tables and p_t products of scalars.
+struct GemmTerm {
+  std::string table;
+  bool transposed = false;
+  std::vector<const Json*> factors;  // scalar factors (names, numbers), in order
+};
+struct GemmPlan {
+  std::string out, J, K;
+  long nj = 0, nk = 0;
+  const Node* nest = nullptr;
+  std::vector<GemmTerm> terms;
+};
+
+bool gemm_plan(const std::vector<Node>& tree, const Emitter& em,
+               const std::map<std::string, const Json*>& tables, GemmPlan& gp) {
+  if (em.e_index.empty() || em.outs.size() != 1 || tree.size() != 1 || !tree[0].loop) return false;
+  const std::vector<Node>& body = tree[0].body;
+  if (body.empty() || !body.back().loop) return false;
+  for (size_t i = 0; i + 1 < body.size(); ++i)
+    if (body[i].loop || em.outs.count(body[i].name) || !em.temps.count(body[i].name) ||
+        !em.temps.at(body[i].name).empty())
+      return false;  // the preheader: scalar temporaries only
+  const Node& Lj = body.back();
+  if (Lj.body.size() != 1 || !Lj.body[0].loop) return false;
+  const Node& Lk = Lj.body[0];
+  if (Lk.body.size() != 1 || Lk.body[0].loop) return false;
+  const Node& st = Lk.body[0];
+  if (Lj.begin != 0 || Lj.end != em.ext.at(Lj.index) || Lk.begin != 0 ||
+      Lk.end != em.ext.at(Lk.index))
+    return false;
+  if (!em.outs.count(st.name) || st.op != "+=" ||
+      st.idx != std::vector<std::string>{em.e_index, Lj.index, Lk.index})
+    return false;
+  gp.out = st.name;
+  gp.J = Lj.index;
+  gp.K = Lk.index;
+  gp.nj = Lj.end;
+  gp.nk = Lk.end;
+  gp.nest = &Lj;
+  auto is_pre = [&](const std::string& n) {
+    auto it = tables.find(n);
+    if (it == tables.end()) return false;
+    const Json* pv = it->second->get("provenance");
+    return pv && pv->kind == Json::Str && pv->str == "preevaluated";
+  };
+  auto scalar = [&](const Json& x) {
+    return x.kind == Json::Num ||
+           (x.kind == Json::Str && (em.consts.count(x.str) ||
+                                    (em.temps.count(x.str) && em.temps.at(x.str).empty())));
+  };
+  auto add_term = [&](const Json& x) {
+    GemmTerm t;
+    auto take = [&](const Json& f) {
+      if (f.kind == Json::Arr && f.arr.size() == 4 && f.arr[0].kind == Json::Str &&
+          f.arr[0].str == "sym" && t.table.empty() && is_pre(f.arr[1].str)) {
+        // subscripts name the table's dims in order: [j][k] or (stored transposed) [k][j]
+        const std::vector<std::string> sub{f.arr[2].str, f.arr[3].str};
+        const auto& dd = em.dims.at(f.arr[1].str);
+        if (sub != dd) return false;
+        if (sub != std::vector<std::string>{gp.J, gp.K} && sub != std::vector<std::string>{gp.K, gp.J})
+          return false;
+        t.table = f.arr[1].str;
+        return true;
+      }
+      if (scalar(f)) {
+        t.factors.push_back(&f);
+        return true;
+      }
+      return false;
+    };
+    if (x.kind == Json::Arr && !x.arr.empty() && x.arr[0].kind == Json::Str && x.arr[0].str == "*") {
+      for (size_t i = 1; i < x.arr.size(); ++i)
+        if (!take(x.arr[i])) return false;
+    } else if (!take(x)) {
+      return false;
+    }
+    if (t.table.empty()) return false;
+    gp.terms.push_back(std::move(t));
+    return true;
+  };
+  const Json& r = *st.rhs;
+  if (r.kind == Json::Arr && !r.arr.empty() && r.arr[0].kind == Json::Str && r.arr[0].str == "+") {
+    for (size_t i = 1; i < r.arr.size(); ++i)
+      if (!add_term(r.arr[i])) return false;
+  } else if (!add_term(r)) {
+    return false;
+  }
+  return !gp.terms.empty();
+}
+
 void scan(const std::vector<Node>& nodes, Emitter& em) {
   for (const Node& n : nodes) {
     if (n.loop) {
@@ -645,6 +749,75 @@ void scan(const std::vector<Node>& nodes, Emitter& em) {
       em.temps[n.name] = n.idx;
     }
   }
+}
+
+// The GEMM mapping: a thread-per-cell kernel evaluates the element preheader and
+// writes the term products P[e][t]; the contraction runs in gemm_f64.cu.
+std::unique_ptr<Kernel> generate_gemm(const Json& ir, Emitter& em,
+                                      const std::map<std::string, const Json*>& tables,
+                                      const GemmPlan& gp, std::unique_ptr<Kernel> K,
+                                      const std::vector<Node>& tree) {
+  (void)ir;
+  const int KT = femgpu::gemm_f64_tile_k(), NT = femgpu::gemm_f64_tile_n();
+  K->gemm = true;
+  K->gK = (int)gp.terms.size();
+  K->gKp = (K->gK + KT - 1) / KT * KT;
+  K->gN = (int)(gp.nj * gp.nk);
+  K->gldb = (K->gN + NT - 1) / NT * NT;
+  K->gB.assign((size_t)K->gKp * K->gldb, 0.0);
+  for (int t = 0; t < K->gK; ++t) {
+    const auto& vals = tables.at(gp.terms[t].table)->at("values").arr;
+    const bool kj = em.dims.at(gp.terms[t].table) == std::vector<std::string>{gp.K, gp.J};
+    for (long j = 0; j < gp.nj; ++j)
+      for (long k = 0; k < gp.nk; ++k)
+        K->gB[(size_t)t * K->gldb + j * gp.nk + k] = vals.at(kj ? k * gp.nj + j : j * gp.nk + k).num;
+  }
+  for (const auto& kv : tables) {
+    const Json* pv = kv.second->get("provenance");
+    const bool pre = pv && pv->kind == Json::Str && pv->str == "preevaluated";
+    (pre ? K->preevaluated : K->inputs).push_back(kv.first);
+  }
+  K->outputs.assign(em.outs.begin(), em.outs.end());
+  K->constants.assign(em.consts.begin(), em.consts.end());
+  std::sort(K->inputs.begin(), K->inputs.end());
+  std::sort(K->preevaluated.begin(), K->preevaluated.end());
+  std::vector<Node> pre(tree[0].body.begin(), tree[0].body.end() - 1);  // scalar statements
+  em.lines.push_back("  const long i_" + em.e_index + " = e0_ + (long)blockIdx.x * blockDim.x + threadIdx.x;");
+  em.lines.push_back("  if (i_" + em.e_index + " >= E) return;");
+  em.emit_nodes(pre, 1);
+  const std::string row = "o_P_[(i_" + em.e_index + " - e0_) * " + std::to_string(K->gKp) + " + ";
+  for (int t = 0; t < K->gK; ++t) {
+    Json prod;
+    prod.kind = Json::Arr;
+    Json op;
+    op.kind = Json::Str;
+    op.str = "*";
+    prod.arr.push_back(op);
+    for (const Json* f : gp.terms[t].factors) prod.arr.push_back(*f);
+    std::string e;
+    if (prod.arr.size() == 1) e = "1.0";
+    else if (prod.arr.size() == 2) e = em.expr(prod.arr[1], 0);
+    else e = em.expr(prod, 0);
+    em.lines.push_back("  " + row + std::to_string(t) + "] = " + e + ";");
+  }
+  for (int t = K->gK; t < K->gKp; ++t)
+    em.lines.push_back("  " + row + std::to_string(t) + "] = 0.0;");
+  std::string src = "// generated by libfemgpu (femgpu_ir_create, GEMM mapping) from a femopt kernel IR\n";
+  src += "extern \"C\" __global__ void __launch_bounds__(128) " + K->fn + "(double* __restrict__ o_P_";
+  for (const auto& t : K->inputs) src += ", const double* __restrict__ t_" + ident(t);
+  for (const auto& c : K->constants) src += ", const double c_" + ident(c);
+  src += ", const long e0_, const long E) {\n";
+  for (const auto& kv : em.temps) {
+    if (!kv.second.empty()) irfail("array temporary in a GEMM preheader");
+    src += "  double v_" + ident(kv.first) + ";\n";
+  }
+  for (const auto& l : em.lines) src += l + "\n";
+  src += "}\n";
+  K->source = src;
+  K->dims = em.dims;
+  K->ext = em.ext;
+  K->e_index = em.e_index;
+  return K;
 }
 
 std::unique_ptr<Kernel> generate(const char* json, int strategy) {
@@ -693,6 +866,11 @@ std::unique_ptr<Kernel> generate(const char* json, int strategy) {
       }
     }
 
+  GemmPlan gp;
+  const bool can_gemm = gemm_plan(tree, em, tables, gp);
+  if (strategy == 3 && !can_gemm) irfail("the gemm mapping does not apply to this nest");
+  if (strategy == 3 || (strategy == 0 && can_gemm && (long)gp.terms.size() * gp.nj * gp.nk >= 2048))
+    return generate_gemm(ir, em, tables, gp, std::move(K), tree);
   const bool can_warp = warp_plan(tree, em);
   bool warp = false;
   if (strategy == 0) {
@@ -706,7 +884,7 @@ std::unique_ptr<Kernel> generate(const char* json, int strategy) {
   } else if (strategy == 2) {
     if (!can_warp) irfail("the warp mapping does not apply to this nest");
     warp = true;
-  } else if (strategy != 1) {
+  } else if (strategy != 1 && strategy != 3) {
     irfail("unknown strategy");
   }
   em.warp = warp;
@@ -974,7 +1152,22 @@ int femgpu_ir_create(const char* json, int strategy, femgpu_ir** out) {
 }
 
 void femgpu_ir_free(femgpu_ir* f) {
-  if (f && f->k && f->k->lib) cudaLibraryUnload(f->k->lib);
+  if (f && f->k) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto& kv : f->k->gB_dev) {
+      cudaSetDevice(kv.first);
+      cudaFree(kv.second);
+    }
+    for (auto& kv : f->k->gP_dev) {
+      cudaSetDevice(kv.first);
+      if (kv.second.done) cudaEventSynchronize(kv.second.done);
+      cudaFree(kv.second.p);
+      if (kv.second.done) cudaEventDestroy(kv.second.done);
+    }
+    cudaSetDevice(cur);
+    if (f->k->lib) cudaLibraryUnload(f->k->lib);
+  }
   delete f;
 }
 
@@ -985,7 +1178,7 @@ int femgpu_ir_get_info(const femgpu_ir* f, femgpu_ir_info* info) {
   info->ninputs = (int)K.inputs.size();
   info->nconstants = (int)K.constants.size();
   info->per_cell = K.e_index.empty() ? 0 : 1;
-  info->strategy = K.warp ? 2 : 1;
+  info->strategy = K.gemm ? 3 : K.warp ? 2 : 1;
   return FEMGPU_OK;
 }
 
@@ -1013,9 +1206,69 @@ int femgpu_ir_launch(femgpu_ir* f, long ncells, double* const* outputs, const do
       (!f->k->inputs.empty() && !inputs) || (!f->k->constants.empty() && !constants))
     return bad_arg("bad argument");
   return ir_guard([&] {
-    const auto& K = *f->k;
+    auto& K = *f->k;
     if (!K.e_index.empty() && ncells == 0) return;
     cudaKernel_t kern = loaded(f);
+    if (K.gemm) {
+      cudaStream_t s = static_cast<cudaStream_t>(stream);
+      int dev = 0;
+      cuda_ok(cudaGetDevice(&dev), "cudaGetDevice");
+      double* dB = nullptr;
+      // one P scratch per (kernel, device), handed between launches (any stream) by
+      // an event: this launch's stream waits for the previous launch's last GEMM
+      std::lock_guard<std::mutex> lock(f->mu);
+      auto it = K.gB_dev.find(dev);
+      if (it == K.gB_dev.end()) {
+        cuda_ok(cudaMalloc(&dB, K.gB.size() * sizeof(double)), "cudaMalloc(tables)");
+        cuda_ok(cudaMemcpy(dB, K.gB.data(), K.gB.size() * sizeof(double), cudaMemcpyHostToDevice),
+                "H2D(tables)");
+        K.gB_dev[dev] = dB;
+      } else {
+        dB = it->second;
+      }
+      // P[chunk][Kp], chunks of <= 2^17 cells
+      const long chunk = std::min<long>(ncells, 1L << 17);
+      auto& sc = K.gP_dev[dev];
+      if (!sc.done) cuda_ok(cudaEventCreateWithFlags(&sc.done, cudaEventDisableTiming), "cudaEventCreate");
+      const size_t need = (size_t)chunk * K.gKp;
+      if (sc.n < need) {
+        cuda_ok(cudaEventSynchronize(sc.done), "cudaEventSynchronize");
+        cudaFree(sc.p);
+        sc.p = nullptr;
+        sc.n = 0;
+        cuda_ok(cudaMalloc(&sc.p, need * sizeof(double)), "cudaMalloc(P)");
+        sc.n = need;
+      }
+      cuda_ok(cudaStreamWaitEvent(s, sc.done, 0), "cudaStreamWaitEvent");
+      double* dP = sc.p;
+      long e0 = 0, Eend = 0;
+      std::vector<void*> args;
+      void* pP = dP;
+      std::vector<const void*> ptrs(K.inputs.size());
+      for (size_t i = 0; i < K.inputs.size(); ++i) ptrs[i] = inputs[i];
+      args.push_back(&pP);
+      for (auto& p : ptrs) args.push_back(&p);
+      std::vector<double> cv(K.constants.size());
+      for (size_t i = 0; i < cv.size(); ++i) {
+        cv[i] = constants[i];
+        args.push_back(&cv[i]);
+      }
+      args.push_back(&e0);
+      args.push_back(&Eend);
+      cudaError_t err = cudaSuccess;
+      for (long c0 = 0; c0 < ncells && err == cudaSuccess; c0 += chunk) {
+        e0 = c0;
+        Eend = std::min(ncells, c0 + chunk);
+        const unsigned grid = (unsigned)((Eend - c0 + 127) / 128);
+        err = cudaLaunchKernel((const void*)kern, dim3(grid), dim3(128), args.data(), 0, s);
+        if (err == cudaSuccess)
+          err = femgpu::launch_gemm_f64_acc(Eend - c0, K.gN, K.gK, K.gKp, dP, dB, K.gldb,
+                                            outputs[0] + c0 * (long)K.gN, s);
+      }
+      if (err == cudaSuccess) err = cudaEventRecord(sc.done, s);
+      cuda_ok(err, "GEMM mapping");
+      return;
+    }
     std::vector<void*> args;
     std::vector<const void*> ptrs(K.outputs.size() + K.inputs.size());
     for (size_t i = 0; i < K.outputs.size(); ++i) ptrs[i] = outputs[i];

@@ -29,7 +29,7 @@ import numpy as np
 
 from . import femgpu
 
-STRATEGIES = {"auto": 0, "thread": 1, "warp": 2}
+STRATEGIES = {"auto": 0, "thread": 1, "warp": 2, "gemm": 3}
 
 
 class IRError(ValueError):
@@ -80,7 +80,7 @@ class IRKernel:
         inf = FemgpuIRInfo()
         _check(L.femgpu_ir_get_info(h, C.byref(inf)))
         self.per_cell = bool(inf.per_cell)
-        self.strategy = {1: "thread", 2: "warp"}[inf.strategy]
+        self.strategy = {1: "thread", 2: "warp", 3: "gemm"}[inf.strategy]
         self.outputs = [self._name(0, i) for i in range(inf.noutputs)]
         self.inputs = [self._name(1, i) for i in range(inf.ninputs)]
         self.constants = [self._name(2, i) for i in range(inf.nconstants)]

@@ -224,3 +224,75 @@ def test_femopt_optimized_kernel_on_gpu_matches_fast_path(case):
     A = ref.cpu().numpy()
     rel = np.linalg.norm((got - A).reshape(E, -1), axis=1) / np.linalg.norm(A.reshape(E, -1), axis=1)
     assert rel.max() < 1e-12
+
+
+# ----------------------------------------------------------------------------
+# GEMM mapping of femopt's pre-evaluated (tensor) nests
+# ----------------------------------------------------------------------------
+def _gemm_ok(js):
+    try:
+        emit_cuda.IRKernel(js, strategy="gemm")
+        return True
+    except emit_cuda.IRError:
+        return False
+
+
+GEMM_CASES = [c for c in CASES if _gemm_ok(load(c)[0])]
+
+
+def test_gemm_mapping_applies_to_tensor_plans():
+    # femopt's G-factored (fully pre-evaluated) plans are GEMM-shaped; raw nests are not
+    assert any("gfac_opt" in c for c in GEMM_CASES)
+    assert not any(c.endswith("_raw") for c in GEMM_CASES)
+    for case in FULL_CASES:
+        d = _load_full(case)
+        strat = [emit_cuda.IRKernel(k["ir"]).strategy for k in d["kernels"]]
+        if case in ("c2_tensor",):
+            assert strat == ["gemm"]
+        if case == "c5_unbounded":
+            assert "gemm" in strat
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", GEMM_CASES)
+def test_gemm_mapping_matches_emitted_c(case):
+    pytest.importorskip("torch")
+    js, d, z = load(case)
+    got = emit_cuda.IRKernel(js, strategy="gemm").run_ir_tables(d)
+    for o in d["outputs"]:
+        ref = z[f"emitc_{o}"]
+        g = got[o].reshape(ref.shape)
+        E = int(d["indices"]["e"])
+        G, R = g.reshape(E, -1), ref.reshape(E, -1)
+        rel = np.linalg.norm(G - R, axis=1) / np.linalg.norm(R, axis=1)
+        assert rel.max() < 1e-12, rel.max()
+
+
+@pytest.mark.gpu
+def test_gemm_mapping_chunks_on_the_full_tensor_plan():
+    # femopt's P3 Helmholtz tensor plan (200 pre-evaluated tables of 20x20) through the
+    # GEMM mapping on more cells than one chunk (2^17), against the hand-written kernel
+    torch = pytest.importorskip("torch")
+    from paper_1604_05872_b200 import femgpu
+
+    d = _load_full("c2_tensor")
+    cfg = fe.CONFIGS["c2"]
+    E = (1 << 17) + 77
+    coords, coeffs = fe.cell_inputs(cfg, ncells=E)
+    dev = torch.device("cuda:0")
+    et = {k: torch.from_numpy(v).to(dev) for k, v in ir.e_tables(cfg, coords, coeffs).items()}
+    k = d["kernels"][0]["ir"]
+    K = emit_cuda.IRKernel(k)
+    assert K.strategy == "gemm"
+    inputs = {n: et[n] if n in et else torch.tensor(np.asarray(k["tables"][n]["values"]),
+                                                    device=dev) for n in K.inputs}
+    out = torch.full((E, cfg.n, cfg.n), 0.25, dtype=torch.float64, device=dev)  # += contract
+    K.run({"A": out}, inputs, k.get("constants", {}), E)
+    ref = torch.empty((E, cfg.n, cfg.n), dtype=torch.float64, device=dev)
+    femgpu.Form.from_config(cfg).assemble(torch.from_numpy(coords).to(dev),
+                                          torch.from_numpy(coeffs).to(dev), ref)
+    torch.cuda.synchronize()
+    G = (out - 0.25).reshape(E, -1)
+    R = ref.reshape(E, -1)
+    rel = ((G - R).norm(dim=1) / R.norm(dim=1)).max().item()
+    assert rel < 1e-12, rel

@@ -75,11 +75,11 @@ def test_elasticity_tensor_accumulate_and_ragged():
 
 
 def test_schedule_contract():
-    # Helmholtz has only the tensor schedule, St Venant-Kirchhoff only the
-    # quadrature one; elasticity has both (auto = quadrature, the faster one)
-    with pytest.raises(femgpu.FemgpuError) as e:
-        femgpu.Form.from_config(fe.CONFIGS["c2"], schedule=femgpu.SCHED_QUADRATURE)
-    assert e.value.code == 14
+    # Helmholtz and elasticity have both schedules (AUTO: tensor resp. quadrature,
+    # the faster ones, tests/test_schedule.py); St Venant-Kirchhoff only quadrature
+    f = femgpu.Form.from_config(fe.CONFIGS["c2"], schedule=femgpu.SCHED_QUADRATURE)
+    assert f.info["schedule"] == "quadrature" and f.info["kernel_name"] == "helm_quad_kernel"
+    assert femgpu.Form.from_config(fe.CONFIGS["c2"]).info["kernel_name"] == "helm_tensor_kernel"
     with pytest.raises(femgpu.FemgpuError) as e:
         femgpu.Form.from_config(fe.CONFIGS["c4"], schedule=femgpu.SCHED_TENSOR)
     assert e.value.code == 14
@@ -105,8 +105,17 @@ def test_elasticity_tensor_schedule(name):
 
 
 def test_unsupported_shapes_fail_loudly():
-    # P3 Helmholtz with a P2 coefficient has no kernel instantiation
-    cfg = replace(fe.CONFIGS["c2"], coef_degree=2, coef_ranges=(("f", 10, 1, 0.5, 1.5, 11),))
+    # P3 Helmholtz with a P2 coefficient has no tensor-kernel instantiation: TENSOR
+    # fails loudly, AUTO takes the quadrature kernel (any coefficient degree)
+    cfg = replace(fe.CONFIGS["c2"], N=3, coef_degree=2, coef_ranges=(("f", 10, 1, 0.5, 1.5, 11),))
+    with pytest.raises(femgpu.FemgpuError) as e:
+        femgpu.Form.from_config(cfg, schedule=femgpu.SCHED_TENSOR)
+    assert e.value.code == 14
+    form, A, R = run(cfg, E=97)
+    assert form.info["kernel_name"] == "helm_quad_kernel"
+    assert frob_rel(A, R) < TOL
+    # no vector-form kernel for P1 vector elements (ns = 4)
+    cfg = replace(fe.CONFIGS["c3"], degree=1)
     with pytest.raises(femgpu.FemgpuError) as e:
         femgpu.Form.from_config(cfg)
     assert e.value.code == 14

@@ -65,7 +65,7 @@ def main():
     ap.add_argument("--femopt", action="store_true")
     ap.add_argument("--vectors", action="store_true",
                     help="the element-vector forms (ir.build_vector: load / residuals), raw IR")
-    ap.add_argument("--strategy", default="auto", choices=["auto", "thread", "warp"])
+    ap.add_argument("--strategy", default="auto", choices=["auto", "thread", "warp", "gemm"])
     ap.add_argument("configs", nargs="*", default=["c1", "c2", "c3", "c4", "c5"])
     a = ap.parse_args()
     if not (a.raw or a.femopt or a.vectors):
