@@ -59,12 +59,13 @@ void elas_tensor_tables(int nq, const double* W, const double* D, const double* 
 cudaError_t launch_elas_tensor(long E, const double* coords, const double* coef, const double* tab,
                                double* A, int acc, cudaStream_t s);
 
-// C[M][N] += A[M][K] * B[K][N] on DMMA (gemm_f64.cu): lda a multiple of 16 with zero
-// columns past K, B zero-padded to [ceil16(K)][ldb], ldb a multiple of 64.
+// C[M][N] += A[M][K] * B[K][N] on DMMA (gemm_f64.cu): A [M][lda] (lda a multiple of 16,
+// zero columns past K) or, a_transposed, [ceil16(K)][lda >= M] (zero rows past K);
+// B zero-padded to [ceil16(K)][ldb], ldb a multiple of 64.
 int gemm_f64_tile_n();
 int gemm_f64_tile_k();
 cudaError_t launch_gemm_f64_acc(long M, int N, int K, int lda, const double* A, const double* B,
-                                int ldb, double* C, cudaStream_t s);
+                                int ldb, double* C, cudaStream_t s, bool a_transposed = false);
 
 // Gather / symbolic / numeric global assembly (see global.cu).
 cudaError_t launch_gather(long E, int ncoef, const double* V, const int* cells, const double* coef,

@@ -11,8 +11,9 @@
 // accumulators), K in chunks of 16 staged by cp.async into double-buffered shared
 // tiles with padded strides (A rows 20 doubles, B rows 72: every fragment load of
 // a warp touches each bank pair at most twice, the 2-wavefront minimum of an
-// LDS.64).  A is [M][lda] with lda a multiple of 16 and zero columns past K; B is
-// [Kpad][ldb] zero-padded to the CTA tiles.  Rows of C past M and columns past N
+// LDS.64).  A is [M][lda] with lda a multiple of 16 and zero columns past K, or
+// transposed [Kpad][lda] (zero rows past K); B is [Kpad][ldb] zero-padded to the
+// CTA tiles.  Rows of C past M and columns past N
 // are not touched.
 #include "common.cuh"
 #include "femgpu_internal.h"
@@ -38,12 +39,16 @@ __device__ __forceinline__ void gm_cp16(void* dst, const void* src) {
                : "memory");
 }
 
+template <bool AT>
 __global__ void __launch_bounds__(128) gemm_f64_acc_kernel(long M, int N, int K, int lda,
                                                            const double* __restrict__ A,
                                                            const double* __restrict__ B, int ldb,
                                                            double* __restrict__ C) {
   using namespace gm;
-  __shared__ __align__(16) double sA[2][A_DBL];
+  // AT: A stored transposed, [K][lda] (column m of row k at A[k*lda + m]; the
+  // producer of A writes it coalesced); the A tile is then staged [BK][BM] with
+  // the B tile's padded stride
+  __shared__ __align__(16) double sA[2][AT ? BK * SB : A_DBL];
   __shared__ __align__(16) double sB[2][B_DBL];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -54,14 +59,27 @@ __global__ void __launch_bounds__(128) gemm_f64_acc_kernel(long M, int N, int K,
 
   auto stage = [&](int kc, int buf) {
     // A: 64 rows x 16 doubles = 512 16-byte chunks; B: 16 rows x 64 doubles = 512
-    for (int i = tid; i < BM * BK / 2; i += 128) {
-      const int r = i / (BK / 2), c2 = i % (BK / 2);
-      double* dst = &sA[buf][r * SA + 2 * c2];
-      const long row = m0 + r;
-      if (row < M)
-        gm_cp16(dst, A + row * lda + kc * BK + 2 * c2);
-      else
-        *reinterpret_cast<double2*>(dst) = make_double2(0.0, 0.0);
+    if (AT) {
+      for (int i = tid; i < BK * BM / 2; i += 128) {
+        const int r = i / (BM / 2), c2 = i % (BM / 2);
+        double* dst = &sA[buf][r * SB + 2 * c2];
+        const long col = m0 + 2 * c2;
+        if (col + 1 < M)
+          gm_cp16(dst, A + (long)(kc * BK + r) * lda + col);
+        else
+          *reinterpret_cast<double2*>(dst) =
+              make_double2(col < M ? A[(long)(kc * BK + r) * lda + col] : 0.0, 0.0);
+      }
+    } else {
+      for (int i = tid; i < BM * BK / 2; i += 128) {
+        const int r = i / (BK / 2), c2 = i % (BK / 2);
+        double* dst = &sA[buf][r * SA + 2 * c2];
+        const long row = m0 + r;
+        if (row < M)
+          gm_cp16(dst, A + row * lda + kc * BK + 2 * c2);
+        else
+          *reinterpret_cast<double2*>(dst) = make_double2(0.0, 0.0);
+      }
     }
     for (int i = tid; i < BK * BN / 2; i += 128) {
       const int r = i / (BN / 2), c2 = i % (BN / 2);
@@ -88,15 +106,20 @@ __global__ void __launch_bounds__(128) gemm_f64_acc_kernel(long M, int N, int K,
       asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     }
     __syncthreads();
-    const double* a = sA[buf] + (wm * 32) * SA;
+    const double* a = sA[buf] + (AT ? wm * 32 : (wm * 32) * SA);
     const double* b = sB[buf] + wn * 32;
 #pragma unroll
     for (int k4 = 0; k4 < BK / 4; ++k4) {
       double af[2][2], bf[4];
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        af[i][0] = a[(16 * i + g) * SA + 4 * k4 + t];
-        af[i][1] = a[(16 * i + g + 8) * SA + 4 * k4 + t];
+        if (AT) {
+          af[i][0] = a[(4 * k4 + t) * SB + 16 * i + g];
+          af[i][1] = a[(4 * k4 + t) * SB + 16 * i + g + 8];
+        } else {
+          af[i][0] = a[(16 * i + g) * SA + 4 * k4 + t];
+          af[i][1] = a[(16 * i + g + 8) * SA + 4 * k4 + t];
+        }
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j) bf[j] = b[(4 * k4 + t) * SB + 8 * j + g];
@@ -135,12 +158,16 @@ int gemm_f64_tile_n() { return gm::BN; }
 int gemm_f64_tile_k() { return gm::BK; }
 
 cudaError_t launch_gemm_f64_acc(long M, int N, int K, int lda, const double* A, const double* B,
-                                int ldb, double* C, cudaStream_t s) {
+                                int ldb, double* C, cudaStream_t s, bool a_transposed) {
   if (M <= 0 || N <= 0) return cudaSuccess;
-  if (lda % 2 || ldb % gm::BN || lda < (K + gm::BK - 1) / gm::BK * gm::BK)
-    return cudaErrorInvalidValue;
+  if (lda % 2 || ldb % gm::BN) return cudaErrorInvalidValue;
+  if (!a_transposed && lda < (K + gm::BK - 1) / gm::BK * gm::BK) return cudaErrorInvalidValue;
+  if (a_transposed && lda < M) return cudaErrorInvalidValue;
   const dim3 grid((unsigned)((M + gm::BM - 1) / gm::BM), (unsigned)((N + gm::BN - 1) / gm::BN));
-  gemm_f64_acc_kernel<<<grid, 128, 0, s>>>(M, N, K, lda, A, B, ldb, C);
+  if (a_transposed)
+    gemm_f64_acc_kernel<true><<<grid, 128, 0, s>>>(M, N, K, lda, A, B, ldb, C);
+  else
+    gemm_f64_acc_kernel<false><<<grid, 128, 0, s>>>(M, N, K, lda, A, B, ldb, C);
   return cudaGetLastError();
 }
 

@@ -785,7 +785,11 @@ std::unique_ptr<Kernel> generate_gemm(const Json& ir, Emitter& em,
   em.lines.push_back("  const long i_" + em.e_index + " = e0_ + (long)blockIdx.x * blockDim.x + threadIdx.x;");
   em.lines.push_back("  if (i_" + em.e_index + " >= E) return;");
   em.emit_nodes(pre, 1);
-  const std::string row = "o_P_[(i_" + em.e_index + " - e0_) * " + std::to_string(K->gKp) + " + ";
+  // P stored transposed, [Kp][ldp] (ldp = cells per chunk): each term's stores are
+  // consecutive across the threads of a warp
+  auto row = [&](int t) {
+    return "o_P_[(long)" + std::to_string(t) + " * ldp_ + (i_" + em.e_index + " - e0_)";
+  };
   for (int t = 0; t < K->gK; ++t) {
     Json prod;
     prod.kind = Json::Arr;
@@ -798,15 +802,14 @@ std::unique_ptr<Kernel> generate_gemm(const Json& ir, Emitter& em,
     if (prod.arr.size() == 1) e = "1.0";
     else if (prod.arr.size() == 2) e = em.expr(prod.arr[1], 0);
     else e = em.expr(prod, 0);
-    em.lines.push_back("  " + row + std::to_string(t) + "] = " + e + ";");
+    em.lines.push_back("  " + row(t) + "] = " + e + ";");
   }
-  for (int t = K->gK; t < K->gKp; ++t)
-    em.lines.push_back("  " + row + std::to_string(t) + "] = 0.0;");
+  for (int t = K->gK; t < K->gKp; ++t) em.lines.push_back("  " + row(t) + "] = 0.0;");
   std::string src = "// generated by libfemgpu (femgpu_ir_create, GEMM mapping) from a femopt kernel IR\n";
   src += "extern \"C\" __global__ void __launch_bounds__(128) " + K->fn + "(double* __restrict__ o_P_";
   for (const auto& t : K->inputs) src += ", const double* __restrict__ t_" + ident(t);
   for (const auto& c : K->constants) src += ", const double c_" + ident(c);
-  src += ", const long e0_, const long E) {\n";
+  src += ", const long e0_, const long E, const long ldp_) {\n";
   for (const auto& kv : em.temps) {
     if (!kv.second.empty()) irfail("array temporary in a GEMM preheader");
     src += "  double v_" + ident(kv.first) + ";\n";
@@ -1230,7 +1233,7 @@ int femgpu_ir_launch(femgpu_ir* f, long ncells, double* const* outputs, const do
       const long chunk = std::min<long>(ncells, 1L << 17);
       auto& sc = K.gP_dev[dev];
       if (!sc.done) cuda_ok(cudaEventCreateWithFlags(&sc.done, cudaEventDisableTiming), "cudaEventCreate");
-      const size_t need = (size_t)chunk * K.gKp;
+      const size_t need = (size_t)((chunk + 1) / 2 * 2) * K.gKp;
       if (sc.n < need) {
         cuda_ok(cudaEventSynchronize(sc.done), "cudaEventSynchronize");
         cudaFree(sc.p);
@@ -1253,8 +1256,10 @@ int femgpu_ir_launch(femgpu_ir* f, long ncells, double* const* outputs, const do
         cv[i] = constants[i];
         args.push_back(&cv[i]);
       }
+      long ldp = (chunk + 1) / 2 * 2;
       args.push_back(&e0);
       args.push_back(&Eend);
+      args.push_back(&ldp);
       cudaError_t err = cudaSuccess;
       for (long c0 = 0; c0 < ncells && err == cudaSuccess; c0 += chunk) {
         e0 = c0;
@@ -1262,8 +1267,8 @@ int femgpu_ir_launch(femgpu_ir* f, long ncells, double* const* outputs, const do
         const unsigned grid = (unsigned)((Eend - c0 + 127) / 128);
         err = cudaLaunchKernel((const void*)kern, dim3(grid), dim3(128), args.data(), 0, s);
         if (err == cudaSuccess)
-          err = femgpu::launch_gemm_f64_acc(Eend - c0, K.gN, K.gK, K.gKp, dP, dB, K.gldb,
-                                            outputs[0] + c0 * (long)K.gN, s);
+          err = femgpu::launch_gemm_f64_acc(Eend - c0, K.gN, K.gK, (int)ldp, dP, dB, K.gldb,
+                                            outputs[0] + c0 * (long)K.gN, s, true);
       }
       if (err == cudaSuccess) err = cudaEventRecord(sc.done, s);
       cuda_ok(err, "GEMM mapping");
