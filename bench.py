@@ -598,10 +598,13 @@ def time_config(args, name, rank, world, local, peaks, pcie):
                "numa_local_cpus": len(cpus) if cpus else None}
         if pcie:
             # ceiling: the copies overlap (two copy engines, full-duplex PCIe) and the
-            # kernel hides behind them -> the slowest of the three, each direction at
-            # the rate it reaches alone (an optimistic floor: pcie_frac <= 1)
-            floor = max(h2d / (pcie["h2d_gbs"] * 1e9), d2h / (pcie["d2h_gbs"] * 1e9),
-                        avg_launch_s)
+            # kernel hides behind them: while both directions stream each runs at the
+            # duplex rate, the rest of the larger one at its rate alone; the kernel
+            # time is the other floor
+            both = min(h2d, d2h)
+            t_copy = both / (pcie["duplex_gbs_each"] * 1e9) + \
+                (h2d - both) / (pcie["h2d_gbs"] * 1e9) + (d2h - both) / (pcie["d2h_gbs"] * 1e9)
+            floor = max(t_copy, avg_launch_s)
             e2e["pcie"] = pcie
             e2e["ceiling"] = cells_all / floor
             e2e["pcie_frac"] = floor / dt
