@@ -34,7 +34,7 @@ from paper_1604_05872_b200 import fe, ir  # noqa: E402
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 # fixture cells per config, and how many of them the (slow) interpreter checks
-CELLS = {"c1": (512, 512), "c2": (32, 8), "c3": (32, 8), "c4": (8, 1), "c5": (8, 2)}
+CELLS = {"c1": (512, 512), "c2": (128, 8), "c3": (128, 16), "c4": (64, 4), "c5": (32, 4)}
 
 
 def frob_rel(a, b):
