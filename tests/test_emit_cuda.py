@@ -296,3 +296,55 @@ def test_gemm_mapping_chunks_on_the_full_tensor_plan():
     R = ref.reshape(E, -1)
     rel = ((G - R).norm(dim=1) / R.norm(dim=1)).max().item()
     assert rel < 1e-12, rel
+
+
+def _synthetic_tensor_ir(E=37, nj=6, nk=5, nt=40, seed=3):
+    """A femopt-shaped pre-evaluated nest: preheader scalars, then
+    OUT[e][j][k] += sum_t T_t * p_t with tables stored [j][k] or [k][j] and products
+    of temporaries, constants and numbers."""
+    rng = np.random.default_rng(seed)
+    tables = {"x0": {"dims": ["e"], "values": list(rng.uniform(0.5, 1.5, E))},
+              "x1": {"dims": ["e"], "values": list(rng.uniform(0.5, 1.5, E))}}
+    stmts = [{"lhs": ["a"], "op": "=", "rhs": ["*", ["sym", "x0", "e"], ["sym", "x1", "e"]]},
+             {"lhs": ["b"], "op": "=", "rhs": ["+", ["sym", "x0", "e"], -0.25]}]
+    terms = []
+    for t in range(nt):
+        name = f"T{t}"
+        if t % 3 == 0:  # stored transposed
+            tables[name] = {"dims": ["k", "j"], "provenance": "preevaluated",
+                            "values": list(rng.uniform(-1, 1, nk * nj))}
+            sym = ["sym", name, "k", "j"]
+        else:
+            tables[name] = {"dims": ["j", "k"], "provenance": "preevaluated",
+                            "values": list(rng.uniform(-1, 1, nj * nk))}
+            sym = ["sym", name, "j", "k"]
+        factors = [sym, "a"] if t % 2 else ["b", sym, "c0", 0.5]
+        terms.append(["*", *factors])
+    nest = {"loop": {"index": "j", "begin": 0, "end": nj, "body": [
+        {"loop": {"index": "k", "begin": 0, "end": nk, "body": [
+            {"lhs": ["A", "e", "j", "k"], "op": "+=", "rhs": ["+", *terms]}]}}]}}
+    return {"indices": {"e": E, "j": nj, "k": nk}, "tables": tables,
+            "constants": {"c0": 1.75}, "outputs": ["A"],
+            "body": [{"loop": {"index": "e", "class": "orderfree", "begin": 0, "end": E,
+                               "body": stmts + [nest]}}]}
+
+
+def test_gemm_mapping_detects_transposed_tables():
+    d = _synthetic_tensor_ir()
+    assert emit_cuda.IRKernel(d, strategy="gemm").strategy == "gemm"
+    assert emit_cuda.IRKernel(d).strategy != "gemm"  # 40 x 30 < 2048 multiply-adds: AUTO keeps thread/warp
+    bad = json.loads(json.dumps(d))
+    bad["body"][0]["loop"]["body"][-1]["loop"]["body"][0]["loop"]["body"][0]["rhs"][1].append(
+        ["sym", "x0", "e"])  # an e-table inside the nest: not a pure tensor contraction
+    with pytest.raises(emit_cuda.IRError):
+        emit_cuda.IRKernel(bad, strategy="gemm")
+
+
+@pytest.mark.gpu
+def test_gemm_mapping_matches_thread_mapping_on_synthetic_plan():
+    pytest.importorskip("torch")
+    d = _synthetic_tensor_ir(E=301)
+    ref = emit_cuda.IRKernel(d, strategy="thread").run_ir_tables(d)["A"].reshape(301, -1)
+    got = emit_cuda.IRKernel(d, strategy="gemm").run_ir_tables(d)["A"].reshape(301, -1)
+    rel = np.linalg.norm(got - ref, axis=1) / np.linalg.norm(ref, axis=1)
+    assert rel.max() < 1e-13
