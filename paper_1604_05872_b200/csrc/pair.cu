@@ -10,8 +10,8 @@
 // only; the same structure, cut for the GPU:
 //
 //  * per (cell, quadrature point q, basis function j) a record of j-side
-//    operands -- g_j = K^T grad phi_j (elasticity), plus h_j = F g_j and
-//    s_j = w' S g_j (St Venant-Kirchhoff) -- computed once per chunk of
+//    operands -- g_j = K^T grad phi_j (elasticity), plus h_j = F g_j
+//    (St Venant-Kirchhoff) -- computed once per chunk of
 //    quadrature points, stored cell-fastest (lanes of one (j,k) tile read
 //    consecutive addresses; j-stride padded so neighbouring tiles of a warp
 //    hit alternate bank halves);
@@ -21,6 +21,13 @@
 //      elasticity  A(c,d) += mu' g_j[d] g_k[c] + lam' g_j[c] g_k[d] + d_cd mu' g_j.g_k
 //      SVK         A(c,d) += lam' h_j[c] h_k[d] + mu' h_k[c] h_j[d]
 //                            + mu' (F F^T)_cd g_j.g_k + d_cd s_j.g_k
+//    where the stress term s_j.g_k = g_k^T (w'S) g_j needs no record of its own:
+//    with S = lam tr(E) I + 2 mu E and 2E = F^T F - I it is
+//      s_j.g_k = sig g_j.g_k + mu' h_j.h_k,   sig = w'(lam tr E - mu)
+//    (sig joins the diagonal of the F F^T coefficients; mu' h_j.h_k is one more
+//    dot product per pair of operands the accumulation loads anyway), so a record
+//    holds g | h (6 doubles) instead of g | h | s (9): 16 % fewer shared-memory
+//    operand loads per (j,k) tile and point, 30 % fewer record stores;
 //  * A_e is symmetric for both forms: only j<=k pairs are accumulated (2x2
 //    register tiles over the upper triangle of the 10x10 (j,k) grid), one
 //    (cell, tile) per accumulating thread, independent FMA passes;
@@ -33,7 +40,7 @@
 //    the records of the next tile into a double buffer (mbarrier full/empty)
 //    while 4 consumer warps accumulate; 2 CTAs per SM;
 //  * pair_svk_ws_kernel (SVK): warp-specialised with a deeper ring -- 4 producer
-//    warps run the heavier per-point setup (F, E, S, F F^T, 10 records per (cell, q))
+//    warps run the heavier per-point setup (F, tr E, F F^T, 10 records per (cell, q))
 //    into a 5-slot ring of 2-point stages while 8 consumer warps (2 cells each)
 //    accumulate; one CTA of 16 cells per SM pools the shared memory for the ring;
 //  * pair_flat_kernel (SVK before, PAIR_SVK_WS=0): every thread takes part in each
@@ -108,8 +115,8 @@ struct PairShape {
   static constexpr int NCOEF = SVK ? 3 * NS + 8 : 8;
   static constexpr int QC = SVK ? PAIR_SVK_QC : Q;       // quadrature points per chunk
   static constexpr int NCHUNK = (Q + QC - 1) / QC;
-  static constexpr int RECD = SVK ? 9 : 3;               // per (q,j): g | h | s
-  static constexpr int QSD = SVK ? 8 : 2;                // per q: lam', mu' | F F^T (6)
+  static constexpr int RECD = SVK ? 6 : 3;               // per (q,j): g | h (SVK), g
+  static constexpr int QSD = SVK ? 8 : 2;                // per q: al, be | F F^T + sig (6)
   // ws (elasticity): each warp owns WCELLS cells of the tile (see pair_slot)
   static constexpr bool WARP_CELLS = !FLAT || PAIR_FLAT_WARP_CELLS;
   static constexpr int WCELLS = CELLS / (ACC / 32);
@@ -253,13 +260,15 @@ __device__ __forceinline__ void pair_point(double (&a4)[2][2][3][3], double (&t1
     // al = (lam'+mu')/2, be = (lam'-mu')/2; the mu' F F^T (g_j.g_k) term is symmetric.
     // a4[c][d] (c<=d) holds the symmetric part (diagonal halved), a4[d][c] (c<d) the
     // antisymmetric one: 27 instead of 33 FP64 instructions per (j,k) pair and point.
-    // qs holds al, be, then mu' F F^T with its diagonal halved (setup).
+    // qs holds al, be, then mu' F F^T with its diagonal halved (setup), the diagonal
+    // carrying sig/2 as well: the sig g_j.g_k part of the stress term s_j.g_k.  Its
+    // other part, mu' h_j.h_k with mu' h_j = al h_j - be h_j, accumulates in t1.
     const double f00 = qs[2 * CELLS], f01 = qs[3 * CELLS], f02 = qs[4 * CELLS];
     const double f11 = qs[5 * CELLS], f12 = qs[6 * CELLS], f22 = qs[7 * CELLS];
     const double ff[3][3] = {{f00, f01, f02}, {f01, f11, f12}, {f02, f12, f22}};
 #pragma unroll
     for (int x = 0; x < 2; ++x) {
-      double gj[3], ah[3], bh[3], s[3];
+      double gj[3], ah[3], bh[3], mh[3];
       const double* r = rq + (j0 + ((PAIR_ABL & 32) ? 0 : x)) * JS;  // 32: timing ablation
 #pragma unroll
       for (int bb = 0; bb < 3; ++bb) {
@@ -267,13 +276,13 @@ __device__ __forceinline__ void pair_point(double (&a4)[2][2][3][3], double (&t1
         const double h = r[(3 + bb) * CELLS];
         ah[bb] = lq * h;                       // al h_j
         bh[bb] = mq * h;                       // be h_j
-        s[bb] = r[(6 + bb) * CELLS];           // w' S g_j
+        mh[bb] = ah[bb] - bh[bb];              // mu' h_j
       }
       double t2[2];
 #pragma unroll
       for (int y = 0; y < 2; ++y) {
-        // s_j.g_k accumulates over q on its own; added to the (c,c) entries once
-        t1[x][y] = fma(s[0], gk[y][0], fma(s[1], gk[y][1], fma(s[2], gk[y][2], t1[x][y])));
+        // mu' h_j.h_k accumulates over q on its own; added to the (c,c) entries once
+        t1[x][y] = fma(mh[0], hk[y][0], fma(mh[1], hk[y][1], fma(mh[2], hk[y][2], t1[x][y])));
         t2[y] = gj[0] * gk[y][0] + gj[1] * gk[y][1] + gj[2] * gk[y][2];
       }
       // first terms: symmetric diagonal and off-diagonal, antisymmetric
@@ -330,8 +339,8 @@ __device__ __forceinline__ void svk_unfold(double (&a4)[2][2][3][3]) {
 }
 
 // Per (cell, quadrature point) setup, one thread: lam', mu' (and, SVK: F = I + grad w,
-// E, w'S, mu' F F^T), then the records of the NS basis functions at q: g_j = K^T D phi_j
-// (elasticity), plus h_j = F g_j and s_j = w' S g_j (SVK).  qs / rec: this cell's
+// tr E, mu' F F^T, sig), then the records of the NS basis functions at q: g_j = K^T D phi_j
+// (elasticity), plus h_j = F g_j (SVK).  qs / rec: this cell's
 // per-point scalars (stride CELLS) and records (j stride JS, component stride CELLS).
 template <bool SVK, int NS, int Q, int CELLS, int JS, int NCOEF, class TW, class TD, class TP>
 __device__ __forceinline__ void pair_point_setup(const double* K, const double* cf, bool valid,
@@ -380,30 +389,22 @@ __device__ __forceinline__ void pair_point_setup(const double* K, const double* 
         F[cc][b] = (cc == b ? 1.0 : 0.0) + gr[0] * Kr[0 * 3 + b] + gr[1] * Kr[1 * 3 + b] +
                    gr[2] * Kr[2 * 3 + b];
     }
-    double Ee[3][3];
+    // tr E, E = (F^T F - I)/2; the stress term s_j.g_k = g_k^T w'S g_j with
+    // S = lam tr(E) I + 2 mu E = (lam tr E - mu) I + mu F^T F becomes
+    // sig g_j.g_k + mu' h_j.h_k, sig = w'(lam tr E - mu), mu' = w' mu (pair_point)
+    double trE = 0.0;
 #pragma unroll
     for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int b = 0; b < 3; ++b) {
-        const double t = F[0][a] * F[0][b] + F[1][a] * F[1][b] + F[2][a] * F[2][b];
-        Ee[a][b] = 0.5 * (a == b ? t - 1.0 : t);
-      }
-    const double trE = Ee[0][0] + Ee[1][1] + Ee[2][2];
-    double Sw[3][3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int b = 0; b < 3; ++b)
-        Sw[a][b] = wq * ((a == b ? lamq * trE : 0.0) + 2.0 * muq * Ee[a][b]);
+      trE += 0.5 * ((F[0][a] * F[0][a] + F[1][a] * F[1][a] + F[2][a] * F[2][a]) - 1.0);
     // mu' F F^T (0,0),(0,1),(0,2),(1,1),(1,2),(2,2), pre-scaled for the accumulate
-    // phase; diagonal halved (svk_unfold)
-    const double mw = muq * wq, mh = 0.5 * mw;
-    qs[2 * CELLS] = mh * (F[0][0] * F[0][0] + F[0][1] * F[0][1] + F[0][2] * F[0][2]);
+    // phase; diagonal halved (svk_unfold) and carrying sig/2
+    const double mw = muq * wq, mh = 0.5 * mw, sh = 0.5 * (wq * (lamq * trE - muq));
+    qs[2 * CELLS] = mh * (F[0][0] * F[0][0] + F[0][1] * F[0][1] + F[0][2] * F[0][2]) + sh;
     qs[3 * CELLS] = mw * (F[0][0] * F[1][0] + F[0][1] * F[1][1] + F[0][2] * F[1][2]);
     qs[4 * CELLS] = mw * (F[0][0] * F[2][0] + F[0][1] * F[2][1] + F[0][2] * F[2][2]);
-    qs[5 * CELLS] = mh * (F[1][0] * F[1][0] + F[1][1] * F[1][1] + F[1][2] * F[1][2]);
+    qs[5 * CELLS] = mh * (F[1][0] * F[1][0] + F[1][1] * F[1][1] + F[1][2] * F[1][2]) + sh;
     qs[6 * CELLS] = mw * (F[1][0] * F[2][0] + F[1][1] * F[2][1] + F[1][2] * F[2][2]);
-    qs[7 * CELLS] = mh * (F[2][0] * F[2][0] + F[2][1] * F[2][1] + F[2][2] * F[2][2]);
+    qs[7 * CELLS] = mh * (F[2][0] * F[2][0] + F[2][1] * F[2][1] + F[2][2] * F[2][2]) + sh;
 #pragma unroll 2
     for (int j = 0; j < NS; ++j) {
       double g[3];
@@ -415,15 +416,12 @@ __device__ __forceinline__ void pair_point_setup(const double* K, const double* 
 #pragma unroll
       for (int b = 0; b < 3; ++b) rr[b * CELLS] = g[b];
 #pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        rr[(3 + a) * CELLS] = F[a][0] * g[0] + F[a][1] * g[1] + F[a][2] * g[2];
-        rr[(6 + a) * CELLS] = Sw[a][0] * g[0] + Sw[a][1] * g[1] + Sw[a][2] * g[2];
-      }
+      for (int a = 0; a < 3; ++a) rr[(3 + a) * CELLS] = F[a][0] * g[0] + F[a][1] * g[1] + F[a][2] * g[2];
     }
   }
 }
 
-// The q-summed scalar term (SVK s_j.g_k, elasticity mu' g_j.g_k) enters the
+// The q-summed scalar term (SVK mu' h_j.h_k, elasticity mu' g_j.g_k) enters the
 // (c,c) entries of each (j,k) pair once.
 __device__ __forceinline__ void add_t1(double (&a4)[2][2][3][3], const double (&t1)[2][2]) {
 #pragma unroll
@@ -714,14 +712,14 @@ __global__ void __launch_bounds__(128, PAIR_FLAT_CTAS)
     }
     __syncthreads();
     double a4[2][2][3][3];
-    double t1[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // SVK: sum_q s_j.g_k; elasticity: mu' g_j.g_k
+    double t1[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // SVK: sum_q mu' h_j.h_k; elasticity: mu' g_j.g_k
     zero_tile(a4);
 #pragma unroll 1
     for (int ch = 0; ch < Sh::NCHUNK; ++ch) {
       const int q0 = ch * Sh::QC;
       const int qn = min(Sh::QC, Q - q0);
-      // ---- per (cell, q), one thread: F = I + grad w, E, w'S, F F^T, lam', mu',
-      //      then the 10 records g_j, h_j = F g_j, s_j = w' S g_j (F, S in registers)
+      // ---- per (cell, q), one thread: F = I + grad w, tr E, F F^T, lam', mu',
+      //      then the 10 records g_j, h_j = F g_j (F in registers)
       // warp-owned cells (JS odd): q and q + 4 share a half-warp, so the record
       // stores of its 16 lanes fall in opposite bank halves
       constexpr int NTASK = Sh::WARP_CELLS ? CELLS * ((Sh::QC + 7) / 8 * 8) : CELLS * Sh::QC;
@@ -789,7 +787,7 @@ struct SvkWsShape {
   static constexpr bool WARP_CELLS = true;
   static constexpr int QS = 32 / CELLS;                 // points per ring stage
   static constexpr int NST = (Q + QS - 1) / QS;         // ring stages per tile
-  static constexpr int RECD = 9, QSD = 8;
+  static constexpr int RECD = 6, QSD = 8;                // g | h; al, be, mu' F F^T + sig
   static constexpr int JS = RECD * CELLS + 1;           // odd: conflict-free warp-cell loads
   static constexpr int STAGE_DBL = QS * (NS * JS + QSD * CELLS);
   static constexpr int NCOEF = 3 * NS + 8;
@@ -851,7 +849,7 @@ __global__ void __launch_bounds__(SvkWsShape<NS, Q>::THREADS, SvkWsShape<NS, Q>:
       const long c0 = (blockIdx.x + it * gridDim.x) * CELLS;
       const int nt = (int)min((long)CELLS, E - c0);
       double a4[2][2][3][3];
-      double t1[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // sum_q s_j.g_k
+      double t1[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // sum_q mu' h_j.h_k
       zero_tile(a4);
 #pragma unroll 1
       for (int st = 0; st < Sh::NST; ++st, ++g) {
