@@ -767,8 +767,8 @@ struct SvkTables {
 // (one (cell, q) per lane: 32 / CELLS points x CELLS cells per ring stage) into an
 // NPW-slot record ring -- producer warp p fills slot p, so each has NPW - 1 stages
 // of lead -- while the consumer warps accumulate; each consumer warp owns 2 cells
-// (15 (j,k) tiles each) and stages / bulk-stores them one at a time through its own
-// 7.2 KB buffer.  CELLS = 8: 2 CTAs x (4 + NPW) warps per SM; CELLS = 16: one CTA
+// (15 (j,k) tiles each) and stages / bulk-stores both at once through their own
+// 7.2 KB staging rows.  CELLS = 8: 2 CTAs x (4 + NPW) warps per SM; CELLS = 16: one CTA
 // of 8 + NPW warps pooling the shared memory into a deeper ring.
 // ============================================================================
 template <int NS_, int Q>
@@ -791,14 +791,20 @@ struct SvkWsShape {
   static constexpr int JS = RECD * CELLS + 1;           // odd: conflict-free warp-cell loads
   static constexpr int STAGE_DBL = QS * (NS * JS + QSD * CELLS);
   static constexpr int NCOEF = 3 * NS + 8;
+  // coefficient rows padded to an odd stride: the producers' per-(cell, q) reads of
+  // 16 cells' rows are conflict-free (stride 38 was 2-way)
+  static constexpr int CF = NCOEF | 1;
   static constexpr int TAB0 = Q + 3 * Q * NS + 4 * Q;
   static constexpr int TAB = PAIR_SVK_PARAMTAB ? 0 : (TAB0 + 1) / 2 * 2;
   static constexpr int CELLD = 10;
-  static constexpr int IN_DBL = CELLS * (12 + NCOEF);
-  static constexpr int CSTRIDE = N * N;                  // one cell per staging buffer
+  static constexpr int IN_DBL = (CELLS * (12 + CF) + 1) / 2 * 2;
+  // staging: every cell of the tile at stride N*N + 2, so a consumer warp stages both
+  // its cells at once with the lane permutation of pair_slot (conflict-free 16-byte
+  // stores, all 30 lanes busy)
+  static constexpr int CSTRIDE = N * N + 2;
   static constexpr int HEAD = TAB + 2 * (CELLS * CELLD + IN_DBL);  // double-buffered per tile
   static constexpr size_t SMEM = sizeof(double) * ((size_t)HEAD + NSLOT * STAGE_DBL +
-                                                   (ACC / 32) * CSTRIDE) +
+                                                   CELLS * CSTRIDE) +
                                  2 * NSLOT * sizeof(uint64_t);
   static_assert(WCELLS * NTILE <= 32 && QS * CELLS == 32, "lane maps");
   static_assert(HEAD % 2 == 0 && STAGE_DBL % 2 == 0 && CSTRIDE % 2 == 0, "16-byte aligned buffers");
@@ -818,8 +824,8 @@ __global__ void __launch_bounds__(SvkWsShape<NS, Q>::THREADS, SvkWsShape<NS, Q>:
   double* sCell = smem + Sh::TAB;             // [2][CELLS][CELLD]          (producers)
   double* sIn = sCell + 2 * CELLS * Sh::CELLD;  // [2][CELLS][12 | NCOEF]   (producers)
   double* sRing = smem + Sh::HEAD;            // [NSLOT][STAGE_DBL]  producers -> consumers
-  double* sStg = sRing + NSLOT * Sh::STAGE_DBL;  // [consumer warps][CSTRIDE]
-  uint64_t* full = reinterpret_cast<uint64_t*>(sStg + (Sh::ACC / 32) * Sh::CSTRIDE);
+  double* sStg = sRing + NSLOT * Sh::STAGE_DBL;  // [CELLS][CSTRIDE]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStg + CELLS * Sh::CSTRIDE);
   uint64_t* empty = full + NSLOT;
   // stage: rec[(ql*NS + j)*JS + comp*CELLS + cell], then qs[(ql*QSD + x)*CELLS + cell]
 
@@ -843,7 +849,6 @@ __global__ void __launch_bounds__(SvkWsShape<NS, Q>::THREADS, SvkWsShape<NS, Q>:
     // ---------------- consumers ----------------
     const PairSlot sl = pair_slot<Sh>(tid);
     const int lane = tid & 31, warp = tid >> 5;
-    double* stg = sStg + warp * Sh::CSTRIDE;
     long g = 0;  // ring stage counter: slot g % NSLOT, use g / NSLOT
     for (long it = 0; it < my_tiles; ++it) {
       const long c0 = (blockIdx.x + it * gridDim.x) * CELLS;
@@ -874,23 +879,21 @@ __global__ void __launch_bounds__(SvkWsShape<NS, Q>::THREADS, SvkWsShape<NS, Q>:
       }
       svk_unfold(a4);
       add_t1(a4, t1);
-      // this warp's cells, one at a time through its staging buffer
-#pragma unroll 1
-      for (int cc = 0; cc < Sh::WCELLS; ++cc) {
-        const int cell = warp * Sh::WCELLS + cc;
-        if (lane == 0) bulk_wait_read0();  // the previous bulk store has read the buffer
-        __syncwarp();
-        if (sl.active && sl.cell == cell) pair_stage<Sh>(stg, a4, sl);
-        fence_proxy_async();
-        __syncwarp();
-        if (lane == 0 && cell < nt) {
+      // this warp's two cells at once through their staging rows
+      if (lane == 0) bulk_wait_read0();  // the previous tile's bulk stores have read them
+      __syncwarp();
+      if (sl.active) pair_stage<Sh>(sStg + sl.cell * Sh::CSTRIDE, a4, sl);
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        for (int cell = warp * Sh::WCELLS; cell < min(warp * Sh::WCELLS + Sh::WCELLS, nt); ++cell) {
           double* dst = A + (c0 + cell) * (size_t)Sh::N * Sh::N;
           if (acc)
-            bulk_s2g_add(dst, stg, Sh::N * Sh::N * 8);
+            bulk_s2g_add(dst, sStg + cell * Sh::CSTRIDE, Sh::N * Sh::N * 8);
           else
-            bulk_s2g(dst, stg, Sh::N * Sh::N * 8);
-          bulk_commit();
+            bulk_s2g(dst, sStg + cell * Sh::CSTRIDE, Sh::N * Sh::N * 8);
         }
+        bulk_commit();
       }
     }
     if (lane == 0) bulk_wait0();
@@ -904,7 +907,8 @@ __global__ void __launch_bounds__(SvkWsShape<NS, Q>::THREADS, SvkWsShape<NS, Q>:
       double* in = sIn + (it & 1) * Sh::IN_DBL;
       for (int i = ptid; i < nt * 12; i += Sh::PROD) cp_async8(&in[i], coords + c0 * 12 + i);
       for (int i = ptid; i < nt * Sh::NCOEF; i += Sh::PROD)
-        cp_async8(&in[CELLS * 12 + i], coef + c0 * Sh::NCOEF + i);
+        cp_async8(&in[CELLS * 12 + (i / Sh::NCOEF) * Sh::CF + i % Sh::NCOEF],
+                  coef + c0 * Sh::NCOEF + i);
       asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
     prefetch(0);
@@ -945,7 +949,7 @@ __global__ void __launch_bounds__(SvkWsShape<NS, Q>::THREADS, SvkWsShape<NS, Q>:
           double* qsp = rec + Sh::QS * NS * Sh::JS + ql * Sh::QSD * CELLS + c;
           double* rp = rec + ql * NS * Sh::JS + c;
           const double* Kc = cell + c * Sh::CELLD;
-          const double* cf = in + CELLS * 12 + c * Sh::NCOEF;
+          const double* cf = in + CELLS * 12 + c * Sh::CF;
           if constexpr (PAIR_SVK_PARAMTAB)
             pair_point_setup<true, NS, Q, CELLS, Sh::JS, Sh::NCOEF>(Kc, cf, c < nt, q, ptab.W,
                                                                    ptab.D, ptab.P, qsp, rp);
