@@ -83,7 +83,7 @@
 #define PAIR_SVK_SLOTS 5  // SVK ws: record ring slots (0: one per producer warp)
 #endif
 #ifndef PAIR_SVK_PW
-#define PAIR_SVK_PW 4  // SVK ws: producer warps
+#define PAIR_SVK_PW 3  // SVK ws: producer warps that build ring stages (of 4)
 #endif
 #ifndef PAIR_SVK_PARAMTAB
 #define PAIR_SVK_PARAMTAB 0  // SVK ws: W | D | P as a kernel parameter (constant bank) instead of
@@ -319,6 +319,73 @@ __device__ __forceinline__ void pair_point(double (&a4)[2][2][3][3], double (&t1
   }
 }
 
+// SVK, one diagonal 2x2 tile (j0 = k0) of the ring kernel: the k side is the j side,
+// so a point needs 12 record loads (g, h of j0, j0+1) and the 8 point scalars instead
+// of 32, and only the pairs (j0,j0), (j0,j0+1), (j0+1,j0+1) are accumulated (87 FP64
+// instructions against 126).  A self pair (j,j) has no antisymmetric part; a4[1][0]
+// and t1[1][0] stay unused (pair_stage writes the (j0+1, j0) block as the mirror).
+template <class Sh>
+__device__ __forceinline__ void pair_point_diag(double (&a4)[2][2][3][3], double (&t1)[2][2],
+                                                const double* rq, const double* qs, int j0) {
+  constexpr int CELLS = Sh::CELLS, JS = Sh::JS;
+  const double lq = qs[0], mq = qs[CELLS];
+  const double f00 = qs[2 * CELLS], f01 = qs[3 * CELLS], f02 = qs[4 * CELLS];
+  const double f11 = qs[5 * CELLS], f12 = qs[6 * CELLS], f22 = qs[7 * CELLS];
+  const double ff[3][3] = {{f00, f01, f02}, {f01, f11, f12}, {f02, f12, f22}};
+  double g[2][3], h[2][3], ah[2][3], bh[2][3], mh[2][3];
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int bb = 0; bb < 3; ++bb) {
+      g[x][bb] = rq[(j0 + x) * JS + bb * CELLS];
+      h[x][bb] = rq[(j0 + x) * JS + (3 + bb) * CELLS];
+    }
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int bb = 0; bb < 3; ++bb) {
+      ah[x][bb] = lq * h[x][bb];
+      bh[x][bb] = mq * h[x][bb];
+      mh[x][bb] = ah[x][bb] - bh[x][bb];
+    }
+  // self pairs (x, x)
+#pragma unroll
+  for (int x = 0; x < 2; ++x) {
+    t1[x][x] = fma(mh[x][0], h[x][0], fma(mh[x][1], h[x][1], fma(mh[x][2], h[x][2], t1[x][x])));
+    const double t2 = g[x][0] * g[x][0] + g[x][1] * g[x][1] + g[x][2] * g[x][2];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int d = c; d < 3; ++d) {
+        a4[x][x][c][d] = fma(ah[x][c], h[x][d], a4[x][x][c][d]);
+        if (d > c) a4[x][x][c][d] = fma(ah[x][d], h[x][c], a4[x][x][c][d]);
+        a4[x][x][c][d] = fma(t2, ff[c][d], a4[x][x][c][d]);
+      }
+  }
+  // the mixed pair (j0, j0+1): as pair_point
+  {
+    t1[0][1] = fma(mh[0][0], h[1][0], fma(mh[0][1], h[1][1], fma(mh[0][2], h[1][2], t1[0][1])));
+    const double t2 = g[0][0] * g[1][0] + g[0][1] * g[1][1] + g[0][2] * g[1][2];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int d = c; d < 3; ++d) {
+        a4[0][1][c][d] = fma(ah[0][c], h[1][d], a4[0][1][c][d]);
+        if (d > c) a4[0][1][d][c] = fma(bh[0][c], h[1][d], a4[0][1][d][c]);
+      }
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int d = c; d < 3; ++d) {
+        if (d > c) {
+          a4[0][1][c][d] = fma(ah[0][d], h[1][c], a4[0][1][c][d]);
+          a4[0][1][d][c] = fma(-bh[0][d], h[1][c], a4[0][1][d][c]);
+        }
+        a4[0][1][c][d] = fma(t2, ff[c][d], a4[0][1][c][d]);
+      }
+  }
+}
+
 // SVK: symmetric (upper, diagonal halved) / antisymmetric (lower) parts -> the block.
 __device__ __forceinline__ void svk_unfold(double (&a4)[2][2][3][3]) {
 #pragma unroll
@@ -374,6 +441,13 @@ __device__ __forceinline__ void pair_point_setup(const double* K, const double* 
     // al, be of the symmetric / antisymmetric split (pair_point, svk_unfold)
     qs[0 * CELLS] = 0.5 * (lamq + muq) * wq;
     qs[1 * CELLS] = 0.5 * (lamq - muq) * wq;
+    // reference derivatives of the NS basis functions at q, read once for grad w
+    // and the records
+    double dq[3][NS];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int m = 0; m < NS; ++m) dq[a][m] = sD[(a * Q + q) * NS + m];
     double F[3][3];
 #pragma unroll
     for (int cc = 0; cc < 3; ++cc) {
@@ -382,7 +456,7 @@ __device__ __forceinline__ void pair_point_setup(const double* K, const double* 
       for (int m = 0; m < NS; ++m) {
         const double wm = cv(cc * NS + m);
 #pragma unroll
-        for (int a = 0; a < 3; ++a) gr[a] += wm * sD[(a * Q + q) * NS + m];
+        for (int a = 0; a < 3; ++a) gr[a] += wm * dq[a][m];
       }
 #pragma unroll
       for (int b = 0; b < 3; ++b)
@@ -405,13 +479,12 @@ __device__ __forceinline__ void pair_point_setup(const double* K, const double* 
     qs[5 * CELLS] = mh * (F[1][0] * F[1][0] + F[1][1] * F[1][1] + F[1][2] * F[1][2]) + sh;
     qs[6 * CELLS] = mw * (F[1][0] * F[2][0] + F[1][1] * F[2][1] + F[1][2] * F[2][2]);
     qs[7 * CELLS] = mh * (F[2][0] * F[2][0] + F[2][1] * F[2][1] + F[2][2] * F[2][2]) + sh;
-#pragma unroll 2
+#pragma unroll
     for (int j = 0; j < NS; ++j) {
       double g[3];
 #pragma unroll
       for (int b = 0; b < 3; ++b)
-        g[b] = Kr[0 * 3 + b] * sD[(0 * Q + q) * NS + j] + Kr[1 * 3 + b] * sD[(1 * Q + q) * NS + j] +
-               Kr[2 * 3 + b] * sD[(2 * Q + q) * NS + j];
+        g[b] = Kr[0 * 3 + b] * dq[0][j] + Kr[1 * 3 + b] * dq[1][j] + Kr[2 * 3 + b] * dq[2][j];
       double* rr = rec + j * JS;
 #pragma unroll
       for (int b = 0; b < 3; ++b) rr[b * CELLS] = g[b];
@@ -764,12 +837,14 @@ struct SvkTables {
 
 // ============================================================================
 // St Venant-Kirchhoff, warp-specialised: NPW producer warps run the per-point setup
-// (one (cell, q) per lane: 32 / CELLS points x CELLS cells per ring stage) into an
-// NPW-slot record ring -- producer warp p fills slot p, so each has NPW - 1 stages
-// of lead -- while the consumer warps accumulate; each consumer warp owns 2 cells
-// (15 (j,k) tiles each) and stages / bulk-stores both at once through their own
-// 7.2 KB staging rows.  CELLS = 8: 2 CTAs x (4 + NPW) warps per SM; CELLS = 16: one CTA
-// of 8 + NPW warps pooling the shared memory into a deeper ring.
+// (one (cell, q) per lane: 2 points x 16 cells per ring stage) into an NSLOT-slot
+// record ring while 8 consumer warps accumulate.  Consumer lane = (cell, tile): the
+// warp's two (j,k) tiles are warp-uniform, so the 10 off-diagonal 2x2 tiles fill 5
+// warps and the 5 diagonal ones -- whose k side is their j side (pair_point_diag:
+// 20 instead of 32 loads, 87 instead of 126 FP64 instructions per point) -- 3 warps.
+// The tile's 16 cells are staged together and bulk-stored two per warp.  Of the 4
+// producer warps the first only loads inputs and computes the geometry, keeping the
+// sub-partition with two off-diagonal consumer warps free of setup work.
 // ============================================================================
 template <int NS_, int Q>
 struct SvkWsShape {
@@ -781,14 +856,22 @@ struct SvkWsShape {
   static constexpr int CELLS = PAIR_SVK_CELLS;
   static constexpr int NPW = PAIR_SVK_PW;               // producer warps (stage g: warp g % NPW)
   static constexpr int NSLOT = PAIR_SVK_SLOTS > 0 ? PAIR_SVK_SLOTS : NPW;  // ring slots
-  static constexpr int WCELLS = 2;                      // cells per consumer warp
-  static constexpr int ACC = 32 * CELLS / WCELLS, PROD = 32 * NPW, THREADS = ACC + PROD;
+  // consumer warps: lane = (cell, one of the warp's two tiles); the 10 off-diagonal
+  // tiles in NOFFW warps, the 5 diagonal ones (k side = j side) in NDIAGW warps
+  static constexpr int NOFF = NTILE - NJ;
+  static constexpr int NOFFW = NOFF / 2, NDIAGW = (NJ + 1) / 2;
+  static constexpr int ACC = 32 * (NOFFW + NDIAGW);
+  // producer warps: 4, of which the last NPW build the ring stages (stage g: worker
+  // g % NPW); with NPW = 3 the first producer warp only loads inputs and geometry, so
+  // its sub-partition carries the two off-diagonal consumer warps 0 and 4
+  static constexpr int NPROD_W = 4, PW0 = NPROD_W - NPW;
+  static constexpr int PROD = 32 * NPROD_W, THREADS = ACC + PROD;
   static constexpr int CTAS_PER_SM = CELLS == 8 ? 2 : 1;
-  static constexpr bool WARP_CELLS = true;
+  static constexpr bool WARP_CELLS = true;  // pair_stage: diagonal mirror folded
   static constexpr int QS = 32 / CELLS;                 // points per ring stage
   static constexpr int NST = (Q + QS - 1) / QS;         // ring stages per tile
   static constexpr int RECD = 6, QSD = 8;                // g | h; al, be, mu' F F^T + sig
-  static constexpr int JS = RECD * CELLS + 1;           // odd: conflict-free warp-cell loads
+  static constexpr int JS = RECD * CELLS + 1;           // j stride of the records
   static constexpr int STAGE_DBL = QS * (NS * JS + QSD * CELLS);
   static constexpr int NCOEF = 3 * NS + 8;
   // coefficient rows padded to an odd stride: the producers' per-(cell, q) reads of
@@ -798,15 +881,17 @@ struct SvkWsShape {
   static constexpr int TAB = PAIR_SVK_PARAMTAB ? 0 : (TAB0 + 1) / 2 * 2;
   static constexpr int CELLD = 10;
   static constexpr int IN_DBL = (CELLS * (12 + CF) + 1) / 2 * 2;
-  // staging: every cell of the tile at stride N*N + 2, so a consumer warp stages both
-  // its cells at once with the lane permutation of pair_slot (conflict-free 16-byte
-  // stores, all 30 lanes busy)
+  // staging: every cell of the tile at stride N*N + 2 (451 16-byte units: the 8 cells
+  // of a quarter-warp's 16-byte stores hit distinct bank groups); the consumers stage
+  // the whole tile, then each warp bulk-stores two cells
   static constexpr int CSTRIDE = N * N + 2;
   static constexpr int HEAD = TAB + 2 * (CELLS * CELLD + IN_DBL);  // double-buffered per tile
   static constexpr size_t SMEM = sizeof(double) * ((size_t)HEAD + NSLOT * STAGE_DBL +
                                                    CELLS * CSTRIDE) +
                                  2 * NSLOT * sizeof(uint64_t);
-  static_assert(WCELLS * NTILE <= 32 && QS * CELLS == 32, "lane maps");
+  static_assert(CELLS == 16 && QS * CELLS == 32 && NOFF % 2 == 0 && NPW >= 1 && NPW <= 4,
+                "lane maps");
+  static_assert((ACC / 32) * 2 >= CELLS, "two cells' bulk stores per consumer warp");
   static_assert(HEAD % 2 == 0 && STAGE_DBL % 2 == 0 && CSTRIDE % 2 == 0, "16-byte aligned buffers");
 };
 
@@ -847,8 +932,31 @@ __global__ void __launch_bounds__(SvkWsShape<NS, Q>::THREADS, SvkWsShape<NS, Q>:
 
   if (tid < Sh::ACC) {
     // ---------------- consumers ----------------
-    const PairSlot sl = pair_slot<Sh>(tid);
     const int lane = tid & 31, warp = tid >> 5;
+    const bool dwarp = warp >= Sh::NOFFW;  // warp-uniform: diagonal-tile warp
+    PairSlot sl;
+    {
+      sl.cell = lane & 15;
+      int t = 2 * (dwarp ? warp - Sh::NOFFW : warp) + (lane >> 4), TJ = 0, TK = 0;
+      if (dwarp) {
+        sl.active = t < Sh::NJ;
+        TJ = TK = sl.active ? t : 0;
+      } else {  // t-th off-diagonal tile (TJ < TK), row by row
+        sl.active = true;
+        for (int J = 0; J < Sh::NJ; ++J) {
+          const int len = Sh::NJ - 1 - J;
+          if (t < len) {
+            TJ = J;
+            TK = J + 1 + t;
+            break;
+          }
+          t -= len;
+        }
+      }
+      sl.j0 = 2 * TJ;
+      sl.k0 = 2 * TK;
+      sl.diag = dwarp;
+    }
     long g = 0;  // ring stage counter: slot g % NSLOT, use g / NSLOT
     for (long it = 0; it < my_tiles; ++it) {
       const long c0 = (blockIdx.x + it * gridDim.x) * CELLS;
@@ -860,18 +968,32 @@ __global__ void __launch_bounds__(SvkWsShape<NS, Q>::THREADS, SvkWsShape<NS, Q>:
       for (int st = 0; st < Sh::NST; ++st, ++g) {
         const int b = (int)(g % NSLOT);
         mbar_wait(&full[b], (uint32_t)((g / NSLOT) & 1));
-        const double* rec = sRing + b * Sh::STAGE_DBL;
-        const double* qsb = rec + Sh::QS * NS * Sh::JS;
+        const double* rec = sRing + b * Sh::STAGE_DBL + sl.cell;
+        const double* qsb = sRing + b * Sh::STAGE_DBL + Sh::QS * NS * Sh::JS + sl.cell;
+        const int nq = min(Sh::QS, Q - st * Sh::QS);
         if (sl.active && !(PAIR_ABL & 1)) {
-          if (st * Sh::QS + Sh::QS <= Q) {
+          if (dwarp) {
+            if (nq == Sh::QS) {
 #pragma unroll
-            for (int ql = 0; ql < Sh::QS; ++ql)
-              pair_point<Sh>(a4, t1, rec + ql * NS * Sh::JS + sl.cell,
-                            qsb + ql * Sh::QSD * CELLS + sl.cell, sl.j0, sl.k0);
+              for (int ql = 0; ql < Sh::QS; ++ql)
+                pair_point_diag<Sh>(a4, t1, rec + ql * NS * Sh::JS, qsb + ql * Sh::QSD * CELLS,
+                                    sl.j0);
+            } else {
+              for (int ql = 0; ql < nq; ++ql)
+                pair_point_diag<Sh>(a4, t1, rec + ql * NS * Sh::JS, qsb + ql * Sh::QSD * CELLS,
+                                    sl.j0);
+            }
           } else {
-            for (int ql = 0; ql < Q - st * Sh::QS; ++ql)
-              pair_point<Sh>(a4, t1, rec + ql * NS * Sh::JS + sl.cell,
-                            qsb + ql * Sh::QSD * CELLS + sl.cell, sl.j0, sl.k0);
+            if (nq == Sh::QS) {
+#pragma unroll
+              for (int ql = 0; ql < Sh::QS; ++ql)
+                pair_point<Sh>(a4, t1, rec + ql * NS * Sh::JS, qsb + ql * Sh::QSD * CELLS, sl.j0,
+                               sl.k0);
+            } else {
+              for (int ql = 0; ql < nq; ++ql)
+                pair_point<Sh>(a4, t1, rec + ql * NS * Sh::JS, qsb + ql * Sh::QSD * CELLS, sl.j0,
+                               sl.k0);
+            }
           }
         }
         __syncwarp();
@@ -879,14 +1001,15 @@ __global__ void __launch_bounds__(SvkWsShape<NS, Q>::THREADS, SvkWsShape<NS, Q>:
       }
       svk_unfold(a4);
       add_t1(a4, t1);
-      // this warp's two cells at once through their staging rows
-      if (lane == 0) bulk_wait_read0();  // the previous tile's bulk stores have read them
-      __syncwarp();
+      // the tile's cells through their staging rows: every consumer stages its tile,
+      // then warp w bulk-stores cells 2w, 2w+1
+      if (lane == 0) bulk_wait_read0();  // this warp's previous bulk stores have read them
+      named_bar(2, Sh::ACC);
       if (sl.active) pair_stage<Sh>(sStg + sl.cell * Sh::CSTRIDE, a4, sl);
       fence_proxy_async();
-      __syncwarp();
+      named_bar(2, Sh::ACC);
       if (lane == 0) {
-        for (int cell = warp * Sh::WCELLS; cell < min(warp * Sh::WCELLS + Sh::WCELLS, nt); ++cell) {
+        for (int cell = 2 * warp; cell < min(2 * warp + 2, nt); ++cell) {
           double* dst = A + (c0 + cell) * (size_t)Sh::N * Sh::N;
           if (acc)
             bulk_s2g_add(dst, sStg + cell * Sh::CSTRIDE, Sh::N * Sh::N * 8);
@@ -940,7 +1063,7 @@ __global__ void __launch_bounds__(SvkWsShape<NS, Q>::THREADS, SvkWsShape<NS, Q>:
       if (it + 1 < my_tiles) prefetch(it + 1);
 #pragma unroll 1
       for (int st = 0; st < Sh::NST; ++st, ++g) {
-        if ((int)(g % NPW) != pw) continue;
+        if ((int)(g % NPW) != pw - Sh::PW0) continue;  // helper warps (pw < PW0): none
         const int b = (int)(g % NSLOT);
         if (g >= NSLOT) mbar_wait(&empty[b], (uint32_t)((g / NSLOT - 1) & 1));
         double* rec = sRing + b * Sh::STAGE_DBL;
