@@ -72,6 +72,9 @@ typedef enum femgpu_form_kind {
  *               geometry/coefficient factors (preeval.cpp:279-451)
  *   QUADRATURE  per-quadrature-point sharing-eliminated accumulation
  *               (sharing.cpp:409-607)
+ *   QUADRATURE_MMA  the same per-point operands, with the sum over points
+ *               run as dense FP64 tensor-core products per cell (St Venant-
+ *               Kirchhoff: svk_mma.cu) instead of per-pair FMA streams
  * AUTO ranks every kernel this library has for the form by predicted time --
  * the roofline time max(flops / FP64 peak, bytes / HBM bandwidth) of the
  * kernel's own flop and byte counts on the current device, divided by the
@@ -83,7 +86,8 @@ typedef enum femgpu_form_kind {
 typedef enum femgpu_schedule {
   FEMGPU_SCHED_AUTO = 0,
   FEMGPU_SCHED_TENSOR = 1,
-  FEMGPU_SCHED_QUADRATURE = 2
+  FEMGPU_SCHED_QUADRATURE = 2,
+  FEMGPU_SCHED_QUADRATURE_MMA = 3
 } femgpu_schedule;
 
 /* Reference tables of a form: exactly the input tables femopt's IR carries
@@ -115,7 +119,7 @@ typedef struct femgpu_form_info {
 /* One kernel the library could run for a form, with its cost model. */
 typedef struct femgpu_schedule_info {
   char kernel_name[64];
-  int schedule;                  /* FEMGPU_SCHED_TENSOR or FEMGPU_SCHED_QUADRATURE */
+  int schedule;                  /* FEMGPU_SCHED_TENSOR, _QUADRATURE or _QUADRATURE_MMA */
   int pipe;                      /* FP64 pipe: 0 = DFMA (CUDA cores), 1 = DMMA (tensor) */
   double flops_per_cell;         /* FP64 flops the kernel executes per cell */
   double bytes_per_cell;         /* compulsory HBM bytes per cell */

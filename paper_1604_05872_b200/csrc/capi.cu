@@ -63,7 +63,8 @@ enum Route {
   ROUTE_HELM_QUAD,
   ROUTE_PAIR,
   ROUTE_ELAS_TENSOR,
-  ROUTE_BURGERS
+  ROUTE_BURGERS,
+  ROUTE_SVK_MMA
 };
 
 std::string two(int m) {
@@ -328,7 +329,7 @@ void validate(const femgpu_form_desc* d) {
     throw Error(FEMGPU_ERR_INCONSISTENT_LAYOUT, "mu and lambda must be P1 (nc == 4)");
   if (d->kind == FEMGPU_BURGERS && !(d->consts[1] != 0.0))
     throw Error(FEMGPU_ERR_INVALID_ARG, "Burgers needs dt != 0 (consts[1])");
-  if (d->schedule < FEMGPU_SCHED_AUTO || d->schedule > FEMGPU_SCHED_QUADRATURE)
+  if (d->schedule < FEMGPU_SCHED_AUTO || d->schedule > FEMGPU_SCHED_QUADRATURE_MMA)
     throw Error(FEMGPU_ERR_INVALID_ARG, "unknown schedule");
 }
 
@@ -382,7 +383,8 @@ Peaks device_peaks() {
 // profiles/schedule_choice_r02.json, tools/sched_compare.py).  The quadrature
 // Helmholtz kernel maps one warp per 4x4 (j,k) tile: ns = 4 keeps one of 16 warps busy.
 constexpr double kEffHelmP1 = 0.831, kEffHelmTensor = 0.754, kEffPairElas = 0.726,
-                 kEffElasTensor = 0.381, kEffPairSvk = 0.432, kEffBurgers = 0.589;
+                 kEffElasTensor = 0.381, kEffPairSvk = 0.505, kEffBurgers = 0.589,
+                 kEffSvkMma = 0.458;
 double eff_helm_quad(int ns) { return ns >= 20 ? 0.245 : ns >= 10 ? 0.2 : 0.04; }
 
 std::vector<Cand> candidates(const femgpu_form_desc* d) {
@@ -419,10 +421,20 @@ std::vector<Cand> candidates(const femgpu_form_desc* d) {
                      "elas_tensor_kernel"});
       break;
     case FEMGPU_HYPERELASTICITY:
-      if (femgpu::pair_supported(d->kind, Q, ns))
+      if (femgpu::pair_supported(d->kind, Q, ns)) {
+        // per point: setup (coefficients, F, tr E, F F^T, g_j, h_j ~ 340 FMA); per (j,k)
+        // 2x2 tile 126 FP64 instructions off the diagonal, 87 on it
+        const int nj = ns / 2;
         c.push_back({ROUTE_PAIR, FEMGPU_SCHED_QUADRATURE, 0,
-                     60 + Q * (ns * 3 * 5 + 16 + ns * (ns + 1) / 2 * 33.0 * 2), kEffPairSvk,
+                     60 + Q * 2.0 * (340 + nj * (nj - 1) / 2 * 126 + nj * 87), kEffPairSvk,
                      "pair_svk_ws_kernel"});
+      }
+      if (femgpu::svk_mma_supported(Q, ns))
+        // per point: setup (coefficients, F, tr E, m_cd ~ 160), g_j, h_j (2 x 90) and the
+        // 55 G_jk (165) as FMAs; per 4-point stage 27 DMMA.8x8x4 (Ylam, Ymu upper tiles, W)
+        c.push_back({ROUTE_SVK_MMA, FEMGPU_SCHED_QUADRATURE_MMA, 1,
+                     60 + Q * 2.0 * (160 + 180 + 165) + (Q + 3) / 4 * 27 * 512.0, kEffSvkMma,
+                     "svk_mma_kernel"});
       break;
     case FEMGPU_BURGERS:
       if (femgpu::burgers_supported(Q, ns)) {
@@ -491,6 +503,9 @@ void launch(const femgpu_form* f, long E, const double* coords, const double* co
       break;
     case ROUTE_ELAS_TENSOR:
       e = femgpu::launch_elas_tensor(E, coords, coef, f->d_tab, A, acc, s);
+      break;
+    case ROUTE_SVK_MMA:
+      e = femgpu::launch_svk_mma(f->nq, f->ns, E, coords, coef, f->d_tab, A, acc, s);
       break;
     case ROUTE_BURGERS:
       e = femgpu::launch_burgers(f->ns, E, coords, coef, f->d_tab, f->consts[0], f->consts[1], A,
@@ -575,6 +590,7 @@ int femgpu_form_create(const femgpu_form_desc* d, femgpu_form** out) {
         femgpu::elas_tensor_tables(f->nq, f->W.data(), f->D.data(), f->P.data(), host.data());
         break;
       case ROUTE_PAIR:  // W | D | P
+      case ROUTE_SVK_MMA:
         host.insert(host.end(), f->W.begin(), f->W.end());
         host.insert(host.end(), f->D.begin(), f->D.end());
         host.insert(host.end(), f->P.begin(), f->P.end());

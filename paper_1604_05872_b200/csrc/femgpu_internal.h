@@ -52,6 +52,13 @@ cudaError_t launch_pair(int kind, int nq, int ns, long E, const double* coords,
                         const double* coef, const double* tab, const double* htab, double* A,
                         int acc, cudaStream_t s);
 
+// St Venant-Kirchhoff on the FP64 tensor cores (see svk_mma.cu): per cell two
+// symmetric rank-1-per-point products and one 6 x 55 product over the quadrature
+// points.  tab = [W(Q) | D(3,Q,ns) | P(Q,4)] as for launch_pair.
+bool svk_mma_supported(int nq, int ns);
+cudaError_t launch_svk_mma(int nq, int ns, long E, const double* coords, const double* coef,
+                           const double* tab, double* A, int acc, cudaStream_t s);
+
 // Linear elasticity tensor schedule (see elasticity.cu).
 bool elas_tensor_supported(int ns, int nc);
 size_t elas_tensor_table_doubles();

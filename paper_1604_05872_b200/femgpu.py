@@ -28,8 +28,9 @@ from . import fe
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libfemgpu.so")
 
-SCHED_AUTO, SCHED_TENSOR, SCHED_QUADRATURE = 0, 1, 2
-SCHEDULE_NAMES = {SCHED_AUTO: "auto", SCHED_TENSOR: "tensor", SCHED_QUADRATURE: "quadrature"}
+SCHED_AUTO, SCHED_TENSOR, SCHED_QUADRATURE, SCHED_QUADRATURE_MMA = 0, 1, 2, 3
+SCHEDULE_NAMES = {SCHED_AUTO: "auto", SCHED_TENSOR: "tensor", SCHED_QUADRATURE: "quadrature",
+                  SCHED_QUADRATURE_MMA: "quadrature_mma"}
 
 ERROR_NAMES = {
     0: "OK", 1: "PARSE", 2: "UNKNOWN_LOOP", 3: "NOT_FEM_NEST", 4: "NON_DISTRIBUTABLE",

@@ -74,6 +74,36 @@ def test_elasticity_tensor_accumulate_and_ragged():
         assert frob_rel(out.cpu().numpy() - 1.5, R) < 1e-11
 
 
+@pytest.mark.parametrize("name", ["c4", "svk_q8"])
+def test_svk_tensor_core_quadrature(name):
+    # St Venant-Kirchhoff with the sum over points on the DMMA pipe (svk_mma.cu), on
+    # request: several 8-cell tiles per CTA (E > 148 x 8) with a ragged last tile,
+    # the accumulate contract and ragged small meshes
+    import port
+
+    cfg = fe.CONFIGS["c4"] if name == "c4" else VARIANTS[name]
+    tabs = fe.tables(cfg)
+    form = femgpu.Form.from_config(cfg, tabs, schedule=femgpu.SCHED_QUADRATURE_MMA)
+    assert form.info["kernel_name"] == "svk_mma_kernel"
+    assert form.info["schedule"] == "quadrature_mma"
+    dev = torch.device("cuda:0")
+    for E in ((1, 7, 9, 3 * 148 * 8 + 5) if name == "c4" else (1, 13, 383)):
+        coords, coeffs = fe.cell_inputs(cfg, ncells=E)
+        R = port.assemble(cfg, tabs, coords, coeffs)
+        x = torch.from_numpy(coords).to(dev)
+        c = torch.from_numpy(coeffs).to(dev)
+        out = torch.empty((E, cfg.n, cfg.n), dtype=torch.float64, device=dev)
+        form.assemble(x, c, out)
+        torch.cuda.synchronize()
+        A = out.cpu().numpy()
+        assert frob_rel(A, R) < TOL, E
+        assert np.array_equal(A, A.transpose(0, 2, 1))
+        out.fill_(1.5)
+        form.assemble(x, c, out, accumulate=True)
+        torch.cuda.synchronize()
+        assert frob_rel(out.cpu().numpy() - 1.5, R) < 1e-11, E
+
+
 def test_schedule_contract():
     # Helmholtz and elasticity have both schedules (AUTO: tensor resp. quadrature,
     # the faster ones, tests/test_schedule.py); St Venant-Kirchhoff only quadrature
@@ -86,7 +116,11 @@ def test_schedule_contract():
     f = femgpu.Form.from_config(fe.CONFIGS["c2"], schedule=femgpu.SCHED_TENSOR)
     assert f.info["schedule"] == "tensor"
     f = femgpu.Form.from_config(fe.CONFIGS["c4"], schedule=femgpu.SCHED_QUADRATURE)
-    assert f.info["schedule"] == "quadrature"
+    assert f.info["schedule"] == "quadrature" and f.info["kernel_name"] == "pair_svk_ws_kernel"
+    f = femgpu.Form.from_config(fe.CONFIGS["c4"], schedule=femgpu.SCHED_QUADRATURE_MMA)
+    assert f.info["schedule"] == "quadrature_mma" and f.info["kernel_name"] == "svk_mma_kernel"
+    with pytest.raises(femgpu.FemgpuError):
+        femgpu.Form.from_config(fe.CONFIGS["c2"], schedule=femgpu.SCHED_QUADRATURE_MMA)
     f = femgpu.Form.from_config(fe.CONFIGS["c3"])
     assert f.info["schedule"] == "quadrature"
     f = femgpu.Form.from_config(fe.CONFIGS["c3"], schedule=femgpu.SCHED_TENSOR)

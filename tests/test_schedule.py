@@ -118,7 +118,7 @@ def test_quadrature_kernel_ragged_and_accumulate():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
 def test_auto_choice_is_the_faster_measured(name):
     """On the BASELINE mesh, the kernel AUTO picks runs faster than the other
     schedule's kernel (timed with CUDA events over a CUDA-graph replay)."""
@@ -131,7 +131,9 @@ def test_auto_choice_is_the_faster_measured(name):
     c = torch.from_numpy(coeffs).to(dev)
     out = torch.empty((coords.shape[0], cfg.n, cfg.n), dtype=torch.float64, device=dev)
     times = {}
-    for sched in (femgpu.SCHED_TENSOR, femgpu.SCHED_QUADRATURE):
+    scheds = ((femgpu.SCHED_QUADRATURE, femgpu.SCHED_QUADRATURE_MMA) if name == "c4"
+              else (femgpu.SCHED_TENSOR, femgpu.SCHED_QUADRATURE))
+    for sched in scheds:
         form = femgpu.Form.from_config(cfg, schedule=sched)
         s = torch.cuda.Stream(dev)
         s.wait_stream(torch.cuda.current_stream(dev))

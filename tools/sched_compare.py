@@ -52,7 +52,7 @@ def main(names):
         ranking = femgpu.schedules(cfg)
         rows = []
         for cand in ranking:
-            sched = femgpu.SCHED_TENSOR if cand["schedule"] == "tensor" else femgpu.SCHED_QUADRATURE
+            sched = {v: k for k, v in femgpu.SCHEDULE_NAMES.items()}[cand["schedule"]]
             form = femgpu.Form.from_config(cfg, schedule=sched)
             if form.info["kernel_name"] != cand["kernel"]:
                 continue  # another kernel of the same schedule ranks first
