@@ -233,7 +233,7 @@ def f_alg(cfg_name):
 
 
 KERNEL_SOURCES = {"helm_quad": "helm_quad.cu", "helm_": "helmholtz.cu", "pair_": "pair.cu",
-                  "burgers": "burgers.cu", "elas_": "elasticity.cu"}
+                  "burgers": "burgers.cu", "elas_": "elasticity.cu", "svk_mma": "svk_mma.cu"}
 
 
 def kernel_source_sha(kernel_name: str):
@@ -534,7 +534,7 @@ def time_config(args, name, rank, world, local, peaks, pcie):
     bpc = cfg.bytes_per_cell()
     avg_launch_s = (sum(per_launch) / len(per_launch)) / 1e3
     uses_dmma = bool(cap and cap.get("dmma_pipe_pct", 0) > 0) if cap else \
-        form.info["kernel_name"].startswith(("helm_tensor", "burgers", "elas_tensor"))
+        form.info["kernel_name"].startswith(("helm_tensor", "burgers", "elas_tensor", "svk_mma"))
     fp64_peak = peaks["dmma_tflops"] if uses_dmma else peaks["dfma_tflops"]
     pipe = "fp64 DMMA" if uses_dmma else "fp64 DFMA"
     t_fp = F_roof / (fp64_peak * 1e12)
