@@ -40,8 +40,13 @@
 #ifndef SVKM_ABL  // development ablations: bit 0 no DMMA, bit 1 no producer setup, bit 2 no assembly
 #define SVKM_ABL 0
 #endif
+#ifndef SVKM_CELLS
+#define SVKM_CELLS 8  // cells per CTA tile (one consumer warp each): 8 -> one CTA per SM,
+                      // 4 -> two independent CTAs per SM with 8-point stages (measured
+                      // 1.476 vs 1.431 ms on c4: the two rings couple worse to the producers)
+#endif
 #ifndef SVKM_SLOTS
-#define SVKM_SLOTS 4  // ring stages in flight
+#define SVKM_SLOTS (SVKM_CELLS == 8 ? 4 : 2)  // ring stages in flight
 #endif
 
 namespace femgpu {
@@ -51,19 +56,24 @@ template <int Q_>
 struct SvkMmaShape {
   static constexpr int Q = Q_;
   static constexpr int NS = 10, N = 30;
-  static constexpr int CELLS = 8;   // cells per CTA tile: consumer warp w owns cell w
-  static constexpr int QS = 4;      // points per ring stage = one k4 step
+  static constexpr int CELLS = SVKM_CELLS;  // cells per CTA tile: consumer warp w owns cell w
+  static constexpr int CTAS_PER_SM = 8 / CELLS;
+  static constexpr int QS = 32 / CELLS;      // points per ring stage (one producer lane each)
+  static constexpr int KSPS = QS / 4;        // k4 steps per stage
   static constexpr int NST = (Q + QS - 1) / QS;
-  static constexpr int NPW = 4;     // producer warps; stage g is built by warp g % NPW
+  static constexpr int NPW = CELLS / 2;      // producer warps; stage g is built by warp g % NPW
   static constexpr int NSLOT = SVKM_SLOTS;
   static constexpr int ACC = 32 * CELLS, PROD = 32 * NPW, THREADS = ACC + PROD;
   static constexpr int NP = NS * (NS + 1) / 2;  // 55 (j <= k) pairs
   static constexpr int NPT = (NP + 7) / 8;       // 7 column tiles of W
   static constexpr int NYT = 10;                  // upper 8x8 tiles of a 32x32 product
-  // per cell and stage: X [4 row tiles][32] | G [NPT][32] | M [32] | lam', mu' [4][2]
+  // per cell and k4 step: X [4 row tiles][32] | G [NPT][32] | M [32] | lam', mu' [4][2]
   static constexpr int OX = 0, OG = 4 * 32, OM = OG + NPT * 32, OLM = OM + 32;
-  static constexpr int CS0 = OLM + 8;
-  static constexpr int CS = CS0 + ((4 - CS0 % 16) + 16) % 16;  // == 4 mod 16
+  static constexpr int KB0 = OLM + 8;
+  static constexpr int KB = KB0 + ((4 - KB0 % 16) + 16) % 16;  // == 4 mod 16
+  // per cell: KSPS k4 blocks (== 4 resp. 8 mod 16: the producer lanes (cell, point) of a
+  // half-warp store to 16 distinct banks)
+  static constexpr int CS = KSPS * KB;
   static constexpr int STAGE_DBL = CELLS * CS;
   // consumer scratch per warp: Ymu [32][YS] | W [8][56]; the staged element matrix
   // (N*N) aliases it once the scratch has been read
@@ -80,10 +90,11 @@ struct SvkMmaShape {
   static constexpr size_t SMEM =
       sizeof(double) * ((size_t)HEAD + NSLOT * STAGE_DBL + CELLS * SCR) +
       2 * NSLOT * sizeof(uint64_t);
-  static_assert(CS % 16 == 4 && STAGE_DBL % 2 == 0 && HEAD % 2 == 0 && SCR % 2 == 0,
-                "aligned, conflict-free stage layout");
+  static_assert(KB % 16 == 4 && CS % 16 == 4 * KSPS && STAGE_DBL % 2 == 0 && HEAD % 2 == 0 &&
+                    SCR % 2 == 0 && QS % 4 == 0 && NSLOT % NPW == 0,
+                "aligned, conflict-free stage layout; a producer warp owns its ring slots");
   static_assert(SCR >= N * N, "staging fits the scratch");
-  static_assert(SMEM <= 227 * 1024, "shared memory");
+  static_assert(SMEM * CTAS_PER_SM <= 227 * 1024, "shared memory");
 };
 
 __device__ __forceinline__ void dmma8x8x4(double (&c)[2], double a, double b) {
@@ -113,7 +124,7 @@ __device__ __forceinline__ int pair_idx(int j, int k) { return j * 10 - j * (j -
 __device__ __forceinline__ int cd_idx(int c, int d) { return c == 0 ? d : c == 1 ? 2 + d : 5; }
 
 template <int Q>
-__global__ void __launch_bounds__(SvkMmaShape<Q>::THREADS, 1)
+__global__ void __launch_bounds__(SvkMmaShape<Q>::THREADS, SvkMmaShape<Q>::CTAS_PER_SM)
     svk_mma_kernel(long E, const double* __restrict__ coords, const double* __restrict__ coef,
                    const double* __restrict__ tab, double* __restrict__ A, int acc) {
   using Sh = SvkMmaShape<Q>;
@@ -162,7 +173,10 @@ __global__ void __launch_bounds__(SvkMmaShape<Q>::THREADS, 1)
       for (int st = 0; st < Sh::NST; ++st, ++g) {
         const int b = (int)(g % NSLOT);
         mbar_wait(&full[b], (uint32_t)((g / NSLOT) & 1));
-        const double* sg = sRing + b * Sh::STAGE_DBL + w * Sh::CS;
+        const int nks = min(Sh::KSPS, (Q - st * Sh::QS + 3) / 4);
+#pragma unroll 1
+        for (int ks = 0; ks < nks; ++ks) {
+        const double* sg = sRing + b * Sh::STAGE_DBL + w * Sh::CS + ks * Sh::KB;
         const double lam = sg[Sh::OLM + 2 * qi], mu = sg[Sh::OLM + 2 * qi + 1];
         double x[4];
 #pragma unroll
@@ -179,6 +193,7 @@ __global__ void __launch_bounds__(SvkMmaShape<Q>::THREADS, 1)
         } else {  // keep the loads alive
           yl[0][0] += lam * x[0] + mf + x[1] + x[2] + x[3];
           ym[0][0] += mu;
+        }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[b]);
@@ -261,7 +276,8 @@ __global__ void __launch_bounds__(SvkMmaShape<Q>::THREADS, 1)
       asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
     prefetch(0);
-    const int c = pt >> 2, ql = pt & 3;  // (cell, point of the stage)
+    const int c = pt / Sh::QS, qq = pt % Sh::QS;  // (cell, point of the stage)
+    const int ql = qq & 3;                           // point within its k4 step
     long g = 0;
     for (long it = 0; it < my_tiles; ++it) {
       const long c0 = (blockIdx.x + it * gridDim.x) * CELLS;
@@ -290,8 +306,8 @@ __global__ void __launch_bounds__(SvkMmaShape<Q>::THREADS, 1)
         if ((int)(g % Sh::NPW) != pw) continue;
         const int b = (int)(g % NSLOT);
         if (g >= NSLOT) mbar_wait(&empty[b], (uint32_t)((g / NSLOT - 1) & 1));
-        double* sg = sRing + b * Sh::STAGE_DBL + c * Sh::CS;
-        const int q = st * Sh::QS + ql;
+        double* sg = sRing + b * Sh::STAGE_DBL + c * Sh::CS + (qq >> 2) * Sh::KB;
+        const int q = st * Sh::QS + qq;
         if (SVKM_ABL & 2) {
         } else if (q < Q) {
           const double* Kc = cell + c * Sh::CELLD;
@@ -394,7 +410,7 @@ cudaError_t launch_q(long E, const double* coords, const double* coef, const dou
   });
   if (e0 != cudaSuccess) return e0;
   const long ntiles = (E + Sh::CELLS - 1) / Sh::CELLS;
-  const long maxc = (long)num_sms();
+  const long maxc = (long)Sh::CTAS_PER_SM * num_sms();
   const int grid = (int)(ntiles < maxc ? ntiles : maxc);
   kern<<<grid, Sh::THREADS, Sh::SMEM, s>>>(E, coords, coef, tab, A, acc);
   return cudaGetLastError();

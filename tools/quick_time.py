@@ -11,6 +11,7 @@ import torch  # noqa: E402
 from paper_1604_05872_b200 import fe, femgpu  # noqa: E402
 
 GRAPH = int(os.environ.get("QT_GRAPH", "0"))  # >0: time a graph of that many launches
+SCHED = int(os.environ.get("QT_SCHED", "0"))  # femgpu schedule (0 = AUTO)
 if os.environ.get("FEMGPU_LIB"):  # A/B builds (development)
     femgpu.LIB_PATH = os.environ["FEMGPU_LIB"]
 
@@ -22,7 +23,7 @@ def main(names):
         t0 = time.time()
         coords, coeffs = fe.cell_inputs(cfg)
         try:
-            form = femgpu.Form.from_config(cfg)
+            form = femgpu.Form.from_config(cfg, schedule=SCHED)
         except femgpu.FemgpuError as e:
             print(json.dumps({"config": name, "error": str(e)}))
             continue
