@@ -888,7 +888,7 @@ struct SvkWsShape {
   static constexpr int HEAD = TAB + 2 * (CELLS * CELLD + IN_DBL);  // double-buffered per tile
   static constexpr size_t SMEM = sizeof(double) * ((size_t)HEAD + NSLOT * STAGE_DBL +
                                                    CELLS * CSTRIDE) +
-                                 2 * NSLOT * sizeof(uint64_t);
+                                 (2 * NSLOT + 2) * sizeof(uint64_t);
   static_assert(CELLS == 16 && QS * CELLS == 32 && NOFF % 2 == 0 && NPW >= 1 && NPW <= 4,
                 "lane maps");
   static_assert((ACC / 32) * 2 >= CELLS, "two cells' bulk stores per consumer warp");
@@ -912,6 +912,8 @@ __global__ void __launch_bounds__(SvkWsShape<NS, Q>::THREADS, SvkWsShape<NS, Q>:
   double* sStg = sRing + NSLOT * Sh::STAGE_DBL;  // [CELLS][CSTRIDE]
   uint64_t* full = reinterpret_cast<uint64_t*>(sStg + CELLS * Sh::CSTRIDE);
   uint64_t* empty = full + NSLOT;
+  uint64_t* staged = empty + NSLOT;  // every consumer warp has staged the tile
+  uint64_t* sfree = staged + 1;      // the previous tile's bulk stores have read the staging
   // stage: rec[(ql*NS + j)*JS + comp*CELLS + cell], then qs[(ql*QSD + x)*CELLS + cell]
 
   const int tid = threadIdx.x;
@@ -926,6 +928,8 @@ __global__ void __launch_bounds__(SvkWsShape<NS, Q>::THREADS, SvkWsShape<NS, Q>:
       mbar_init(&full[b], 32);
       mbar_init(&empty[b], Sh::ACC / 32);
     }
+    mbar_init(staged, Sh::ACC / 32);
+    mbar_init(sfree, 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -933,6 +937,7 @@ __global__ void __launch_bounds__(SvkWsShape<NS, Q>::THREADS, SvkWsShape<NS, Q>:
   if (tid < Sh::ACC) {
     // ---------------- consumers ----------------
     const int lane = tid & 31, warp = tid >> 5;
+    const bool issuer = tid == 0;  // bulk-stores the tile's 16 cells
     const bool dwarp = warp >= Sh::NOFFW;  // warp-uniform: diagonal-tile warp
     PairSlot sl;
     {
@@ -998,18 +1003,25 @@ __global__ void __launch_bounds__(SvkWsShape<NS, Q>::THREADS, SvkWsShape<NS, Q>:
         }
         __syncwarp();
         if (lane == 0) mbar_arrive_cta(&empty[b]);
+        // halfway through the tile the previous tile's bulk stores have long read the
+        // staging: release it (no consumer warp waits for another at the tile end)
+        if (issuer && it > 0 && st == Sh::NST / 2) {
+          bulk_wait_read0();
+          mbar_arrive_cta(sfree);
+        }
       }
       svk_unfold(a4);
       add_t1(a4, t1);
-      // the tile's cells through their staging rows: every consumer stages its tile,
-      // then warp w bulk-stores cells 2w, 2w+1
-      if (lane == 0) bulk_wait_read0();  // this warp's previous bulk stores have read them
-      named_bar(2, Sh::ACC);
+      // the tile's cells through their staging rows: every consumer warp stages its
+      // tiles and arrives; the issuer bulk-stores the 16 cells once all have
+      if (it > 0) mbar_wait(sfree, (uint32_t)((it - 1) & 1));
       if (sl.active) pair_stage<Sh>(sStg + sl.cell * Sh::CSTRIDE, a4, sl);
       fence_proxy_async();
-      named_bar(2, Sh::ACC);
-      if (lane == 0) {
-        for (int cell = 2 * warp; cell < min(2 * warp + 2, nt); ++cell) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cta(staged);
+      if (issuer) {
+        mbar_wait(staged, (uint32_t)(it & 1));
+        for (int cell = 0; cell < nt; ++cell) {
           double* dst = A + (c0 + cell) * (size_t)Sh::N * Sh::N;
           if (acc)
             bulk_s2g_add(dst, sStg + cell * Sh::CSTRIDE, Sh::N * Sh::N * 8);
@@ -1019,7 +1031,7 @@ __global__ void __launch_bounds__(SvkWsShape<NS, Q>::THREADS, SvkWsShape<NS, Q>:
         bulk_commit();
       }
     }
-    if (lane == 0) bulk_wait0();
+    if (issuer) bulk_wait0();
   } else {
     // ---------------- producer warps: inputs (cp.async, one tile ahead), geometry,
     //                  per-point setup; warp pw takes stages g = pw mod NPW ----------------
