@@ -80,14 +80,17 @@
 #define PAIR_SVK_CELLS 16  // SVK ws: cells per CTA tile (8: 2 CTAs per SM, 16: one)
 #endif
 #ifndef PAIR_SVK_SLOTS
-#define PAIR_SVK_SLOTS 5  // SVK ws: record ring slots (0: one per producer warp)
+#define PAIR_SVK_SLOTS (PAIR_SVK_GREC ? 4 : 5)  // SVK ws: record ring slots (0: one per producer warp)
 #endif
 #ifndef PAIR_SVK_PW
 #define PAIR_SVK_PW 3  // SVK ws: producer warps that build ring stages (of 4)
 #endif
+#ifndef PAIR_SVK_GREC
+#define PAIR_SVK_GREC 1  // SVK ws: records h_j + G_jk (producers do the g_j.g_k) instead of g_j | h_j
+#endif
 #ifndef PAIR_SVK_PARAMTAB
-#define PAIR_SVK_PARAMTAB 0  // SVK ws: W | D | P as a kernel parameter (constant bank) instead of
-                             // smem (measured: 1.263 vs 1.254 ms on c4, not adopted)
+#define PAIR_SVK_PARAMTAB PAIR_SVK_GREC  // SVK ws: W | D | P as a kernel parameter (constant bank)
+                                         // instead of smem (frees 7.6 KB for the G records)
 #endif
 #ifndef PAIR_ABL  // development ablations of pair_ws_kernel: bit 0 no accumulate, bit 1 no store,
                   // bit 2 no records, bit 3 no geometry, bit 4 no staging
@@ -386,6 +389,124 @@ __device__ __forceinline__ void pair_point_diag(double (&a4)[2][2][3][3], double
   }
 }
 
+// SVK ring kernel with G records (PAIR_SVK_GREC): the producers store, per (cell,
+// point), h_j (3 per j) and the 55 G_jk = g_j.g_k instead of g_j | h_j, so a 2x2
+// tile's point reads h of its two j and two k rows, its 4 G values and the 8 point
+// scalars (24 loads instead of 32) and skips the 12 FP64 instructions of its four
+// g_j.g_k; the dot products move to the producer warps, which wait on the ring
+// otherwise.  rq: this cell's h records (j stride JS, component stride CELLS),
+// gq: its G of pairs p (stride CELLS), qs: its point scalars.
+template <class Sh>
+__device__ __forceinline__ void svk_point_g(double (&a4)[2][2][3][3], double (&t1)[2][2],
+                                            const double* rq, const double* gq,
+                                            const double* qs, int j0, int k0,
+                                            const int (&p)[2][2]) {
+  constexpr int CELLS = Sh::CELLS, JS = Sh::JS;
+  const double lq = qs[0], mq = qs[CELLS];
+  const double f00 = qs[2 * CELLS], f01 = qs[3 * CELLS], f02 = qs[4 * CELLS];
+  const double f11 = qs[5 * CELLS], f12 = qs[6 * CELLS], f22 = qs[7 * CELLS];
+  const double ff[3][3] = {{f00, f01, f02}, {f01, f11, f12}, {f02, f12, f22}};
+  double hk[2][3];
+#pragma unroll
+  for (int y = 0; y < 2; ++y)
+#pragma unroll
+    for (int bb = 0; bb < 3; ++bb) hk[y][bb] = rq[(k0 + y) * JS + bb * CELLS];
+#pragma unroll
+  for (int x = 0; x < 2; ++x) {
+    double ah[3], bh[3], mh[3];
+#pragma unroll
+    for (int bb = 0; bb < 3; ++bb) {
+      const double h = rq[(j0 + x) * JS + bb * CELLS];
+      ah[bb] = lq * h;
+      bh[bb] = mq * h;
+      mh[bb] = ah[bb] - bh[bb];
+    }
+    double t2[2];
+#pragma unroll
+    for (int y = 0; y < 2; ++y) {
+      t1[x][y] = fma(mh[0], hk[y][0], fma(mh[1], hk[y][1], fma(mh[2], hk[y][2], t1[x][y])));
+      t2[y] = gq[p[x][y] * CELLS];
+    }
+#pragma unroll
+    for (int y = 0; y < 2; ++y)
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int d = c; d < 3; ++d) {
+          a4[x][y][c][d] = fma(ah[c], hk[y][d], a4[x][y][c][d]);
+          if (d > c) a4[x][y][d][c] = fma(bh[c], hk[y][d], a4[x][y][d][c]);
+        }
+#pragma unroll
+    for (int y = 0; y < 2; ++y)
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int d = c; d < 3; ++d) {
+          if (d > c) {
+            a4[x][y][c][d] = fma(ah[d], hk[y][c], a4[x][y][c][d]);
+            a4[x][y][d][c] = fma(-bh[d], hk[y][c], a4[x][y][d][c]);
+          }
+          a4[x][y][c][d] = fma(t2[y], ff[c][d], a4[x][y][c][d]);
+        }
+  }
+}
+
+// The diagonal tile of svk_point_g (pair_point_diag with G records): 17 loads.
+template <class Sh>
+__device__ __forceinline__ void svk_point_g_diag(double (&a4)[2][2][3][3], double (&t1)[2][2],
+                                                 const double* rq, const double* gq,
+                                                 const double* qs, int j0, const int (&p)[2][2]) {
+  constexpr int CELLS = Sh::CELLS, JS = Sh::JS;
+  const double lq = qs[0], mq = qs[CELLS];
+  const double f00 = qs[2 * CELLS], f01 = qs[3 * CELLS], f02 = qs[4 * CELLS];
+  const double f11 = qs[5 * CELLS], f12 = qs[6 * CELLS], f22 = qs[7 * CELLS];
+  const double ff[3][3] = {{f00, f01, f02}, {f01, f11, f12}, {f02, f12, f22}};
+  double h[2][3], ah[2][3], bh[2][3], mh[2][3];
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int bb = 0; bb < 3; ++bb) {
+      h[x][bb] = rq[(j0 + x) * JS + bb * CELLS];
+      ah[x][bb] = lq * h[x][bb];
+      bh[x][bb] = mq * h[x][bb];
+      mh[x][bb] = ah[x][bb] - bh[x][bb];
+    }
+#pragma unroll
+  for (int x = 0; x < 2; ++x) {
+    t1[x][x] = fma(mh[x][0], h[x][0], fma(mh[x][1], h[x][1], fma(mh[x][2], h[x][2], t1[x][x])));
+    const double t2 = gq[p[x][x] * CELLS];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int d = c; d < 3; ++d) {
+        a4[x][x][c][d] = fma(ah[x][c], h[x][d], a4[x][x][c][d]);
+        if (d > c) a4[x][x][c][d] = fma(ah[x][d], h[x][c], a4[x][x][c][d]);
+        a4[x][x][c][d] = fma(t2, ff[c][d], a4[x][x][c][d]);
+      }
+  }
+  {
+    t1[0][1] = fma(mh[0][0], h[1][0], fma(mh[0][1], h[1][1], fma(mh[0][2], h[1][2], t1[0][1])));
+    const double t2 = gq[p[0][1] * CELLS];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int d = c; d < 3; ++d) {
+        a4[0][1][c][d] = fma(ah[0][c], h[1][d], a4[0][1][c][d]);
+        if (d > c) a4[0][1][d][c] = fma(bh[0][c], h[1][d], a4[0][1][d][c]);
+      }
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int d = c; d < 3; ++d) {
+        if (d > c) {
+          a4[0][1][c][d] = fma(ah[0][d], h[1][c], a4[0][1][c][d]);
+          a4[0][1][d][c] = fma(-bh[0][d], h[1][c], a4[0][1][d][c]);
+        }
+        a4[0][1][c][d] = fma(t2, ff[c][d], a4[0][1][c][d]);
+      }
+  }
+}
+
 // SVK: symmetric (upper, diagonal halved) / antisymmetric (lower) parts -> the block.
 __device__ __forceinline__ void svk_unfold(double (&a4)[2][2][3][3]) {
 #pragma unroll
@@ -492,6 +613,76 @@ __device__ __forceinline__ void pair_point_setup(const double* K, const double* 
       for (int a = 0; a < 3; ++a) rr[(3 + a) * CELLS] = F[a][0] * g[0] + F[a][1] * g[1] + F[a][2] * g[2];
     }
   }
+}
+
+// Per (cell, point) setup of the SVK ring kernel with G records: the point scalars as
+// pair_point_setup, then h_j = F g_j (records, j stride JS) and G_jk = g_j.g_k for the
+// j <= k pairs (gq, pair stride CELLS).  TW/TD/TP: W | D | P tables.
+template <int NS, int Q, int CELLS, int JS, class TW, class TD, class TP>
+__device__ __forceinline__ void svk_setup_g(const double* K, const double* cf, bool valid, int q,
+                                            const TW& sW, const TD& sD, const TP& sP, double* qs,
+                                            double* rec, double* gq) {
+  auto cv = [&](int r) -> double { return valid ? cf[r] : 0.0; };
+  constexpr int CO = 3 * NS;
+  double muq = 0, lamq = 0;
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    muq += cv(CO + m) * sP[q * 4 + m];
+    lamq += cv(CO + 4 + m) * sP[q * 4 + m];
+  }
+  const double wq = sW[q] * K[9];
+  double Kr[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) Kr[i] = K[i];
+  qs[0 * CELLS] = 0.5 * (lamq + muq) * wq;
+  qs[1 * CELLS] = 0.5 * (lamq - muq) * wq;
+  double dq[3][NS];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int m = 0; m < NS; ++m) dq[a][m] = sD[(a * Q + q) * NS + m];
+  double F[3][3];
+#pragma unroll
+  for (int cc = 0; cc < 3; ++cc) {
+    double gr[3] = {0, 0, 0};
+#pragma unroll
+    for (int m = 0; m < NS; ++m) {
+      const double wm = cv(cc * NS + m);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) gr[a] += wm * dq[a][m];
+    }
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+      F[cc][b] = (cc == b ? 1.0 : 0.0) + gr[0] * Kr[0 * 3 + b] + gr[1] * Kr[1 * 3 + b] +
+                 gr[2] * Kr[2 * 3 + b];
+  }
+  double trE = 0.0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+    trE += 0.5 * ((F[0][a] * F[0][a] + F[1][a] * F[1][a] + F[2][a] * F[2][a]) - 1.0);
+  const double mw = muq * wq, mh = 0.5 * mw, sh = 0.5 * (wq * (lamq * trE - muq));
+  qs[2 * CELLS] = mh * (F[0][0] * F[0][0] + F[0][1] * F[0][1] + F[0][2] * F[0][2]) + sh;
+  qs[3 * CELLS] = mw * (F[0][0] * F[1][0] + F[0][1] * F[1][1] + F[0][2] * F[1][2]);
+  qs[4 * CELLS] = mw * (F[0][0] * F[2][0] + F[0][1] * F[2][1] + F[0][2] * F[2][2]);
+  qs[5 * CELLS] = mh * (F[1][0] * F[1][0] + F[1][1] * F[1][1] + F[1][2] * F[1][2]) + sh;
+  qs[6 * CELLS] = mw * (F[1][0] * F[2][0] + F[1][1] * F[2][1] + F[1][2] * F[2][2]);
+  qs[7 * CELLS] = mh * (F[2][0] * F[2][0] + F[2][1] * F[2][1] + F[2][2] * F[2][2]) + sh;
+  double g[NS][3];
+#pragma unroll
+  for (int j = 0; j < NS; ++j) {
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+      g[j][b] = Kr[0 * 3 + b] * dq[0][j] + Kr[1 * 3 + b] * dq[1][j] + Kr[2 * 3 + b] * dq[2][j];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      rec[j * JS + a * CELLS] = F[a][0] * g[j][0] + F[a][1] * g[j][1] + F[a][2] * g[j][2];
+  }
+  int p = 0;
+#pragma unroll
+  for (int j = 0; j < NS; ++j)
+#pragma unroll
+    for (int k = j; k < NS; ++k, ++p)
+      gq[p * CELLS] = g[j][0] * g[k][0] + g[j][1] * g[k][1] + g[j][2] * g[k][2];
 }
 
 // The q-summed scalar term (SVK mu' h_j.h_k, elasticity mu' g_j.g_k) enters the
@@ -870,9 +1061,14 @@ struct SvkWsShape {
   static constexpr bool WARP_CELLS = true;  // pair_stage: diagonal mirror folded
   static constexpr int QS = 32 / CELLS;                 // points per ring stage
   static constexpr int NST = (Q + QS - 1) / QS;         // ring stages per tile
-  static constexpr int RECD = 6, QSD = 8;                // g | h; al, be, mu' F F^T + sig
+  static constexpr bool GREC = PAIR_SVK_GREC;
+  static constexpr int RECD = GREC ? 3 : 6, QSD = 8;   // h (| g); al, be, mu' F F^T + sig
   static constexpr int JS = RECD * CELLS + 1;           // j stride of the records
-  static constexpr int STAGE_DBL = QS * (NS * JS + QSD * CELLS);
+  static constexpr int NP = NS * (NS + 1) / 2;          // (j <= k) pairs: G records
+  static constexpr int GOFF = NS * JS;                  // per point: records | G | scalars
+  static constexpr int QSOFF = GOFF + (GREC ? NP * CELLS : 0);
+  static constexpr int PT_DBL = QSOFF + QSD * CELLS;
+  static constexpr int STAGE_DBL = QS * PT_DBL;
   static constexpr int NCOEF = 3 * NS + 8;
   // coefficient rows padded to an odd stride: the producers' per-(cell, q) reads of
   // 16 cells' rows are conflict-free (stride 38 was 2-way)
@@ -893,7 +1089,13 @@ struct SvkWsShape {
                 "lane maps");
   static_assert((ACC / 32) * 2 >= CELLS, "two cells' bulk stores per consumer warp");
   static_assert(HEAD % 2 == 0 && STAGE_DBL % 2 == 0 && CSTRIDE % 2 == 0, "16-byte aligned buffers");
+  static_assert(SMEM <= 227 * 1024, "shared memory");
 };
+
+// (j <= k) pair index of the G records
+__host__ __device__ constexpr int svk_pair(int ns, int j, int k) {
+  return j * (2 * ns - j + 1) / 2 + (k - j);
+}
 
 template <int NS, int Q>
 __global__ void __launch_bounds__(SvkWsShape<NS, Q>::THREADS, SvkWsShape<NS, Q>::CTAS_PER_SM)
@@ -962,6 +1164,14 @@ __global__ void __launch_bounds__(SvkWsShape<NS, Q>::THREADS, SvkWsShape<NS, Q>:
       sl.k0 = 2 * TK;
       sl.diag = dwarp;
     }
+    int pidx[2][2];  // G record pairs of the tile (diagonal tile: (j0+1, j0) unused)
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+      for (int y = 0; y < 2; ++y) {
+        const int j = sl.j0 + x, k = sl.k0 + y;
+        pidx[x][y] = svk_pair(NS, min(j, k), max(j, k));
+      }
     long g = 0;  // ring stage counter: slot g % NSLOT, use g / NSLOT
     for (long it = 0; it < my_tiles; ++it) {
       const long c0 = (blockIdx.x + it * gridDim.x) * CELLS;
@@ -973,9 +1183,37 @@ __global__ void __launch_bounds__(SvkWsShape<NS, Q>::THREADS, SvkWsShape<NS, Q>:
       for (int st = 0; st < Sh::NST; ++st, ++g) {
         const int b = (int)(g % NSLOT);
         mbar_wait(&full[b], (uint32_t)((g / NSLOT) & 1));
+        const int nq = min(Sh::QS, Q - st * Sh::QS);
+        if constexpr (Sh::GREC) {
+          const double* pt = sRing + b * Sh::STAGE_DBL + sl.cell;  // point ql at ql * PT_DBL
+          if (sl.active && !(PAIR_ABL & 1)) {
+            if (dwarp) {
+              if (nq == Sh::QS) {
+#pragma unroll
+                for (int ql = 0; ql < Sh::QS; ++ql)
+                  svk_point_g_diag<Sh>(a4, t1, pt + ql * Sh::PT_DBL, pt + ql * Sh::PT_DBL + Sh::GOFF,
+                                       pt + ql * Sh::PT_DBL + Sh::QSOFF, sl.j0, pidx);
+              } else {
+                for (int ql = 0; ql < nq; ++ql)
+                  svk_point_g_diag<Sh>(a4, t1, pt + ql * Sh::PT_DBL, pt + ql * Sh::PT_DBL + Sh::GOFF,
+                                       pt + ql * Sh::PT_DBL + Sh::QSOFF, sl.j0, pidx);
+              }
+            } else {
+              if (nq == Sh::QS) {
+#pragma unroll
+                for (int ql = 0; ql < Sh::QS; ++ql)
+                  svk_point_g<Sh>(a4, t1, pt + ql * Sh::PT_DBL, pt + ql * Sh::PT_DBL + Sh::GOFF,
+                                  pt + ql * Sh::PT_DBL + Sh::QSOFF, sl.j0, sl.k0, pidx);
+              } else {
+                for (int ql = 0; ql < nq; ++ql)
+                  svk_point_g<Sh>(a4, t1, pt + ql * Sh::PT_DBL, pt + ql * Sh::PT_DBL + Sh::GOFF,
+                                  pt + ql * Sh::PT_DBL + Sh::QSOFF, sl.j0, sl.k0, pidx);
+              }
+            }
+          }
+        } else {
         const double* rec = sRing + b * Sh::STAGE_DBL + sl.cell;
         const double* qsb = sRing + b * Sh::STAGE_DBL + Sh::QS * NS * Sh::JS + sl.cell;
-        const int nq = min(Sh::QS, Q - st * Sh::QS);
         if (sl.active && !(PAIR_ABL & 1)) {
           if (dwarp) {
             if (nq == Sh::QS) {
@@ -1000,6 +1238,7 @@ __global__ void __launch_bounds__(SvkWsShape<NS, Q>::THREADS, SvkWsShape<NS, Q>:
                                sl.k0);
             }
           }
+        }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive_cta(&empty[b]);
@@ -1080,7 +1319,17 @@ __global__ void __launch_bounds__(SvkWsShape<NS, Q>::THREADS, SvkWsShape<NS, Q>:
         if (g >= NSLOT) mbar_wait(&empty[b], (uint32_t)((g / NSLOT - 1) & 1));
         double* rec = sRing + b * Sh::STAGE_DBL;
         const int q = st * Sh::QS + ql;
-        if (q < Q && !(PAIR_ABL & 4)) {
+        if (q < Q && !(PAIR_ABL & 4) && Sh::GREC) {
+          double* pp = rec + ql * Sh::PT_DBL + c;
+          const double* Kc = cell + c * Sh::CELLD;
+          const double* cf = in + CELLS * 12 + c * Sh::CF;
+          if constexpr (PAIR_SVK_PARAMTAB)
+            svk_setup_g<NS, Q, CELLS, Sh::JS>(Kc, cf, c < nt, q, ptab.W, ptab.D, ptab.P,
+                                             pp + Sh::QSOFF, pp, pp + Sh::GOFF);
+          else
+            svk_setup_g<NS, Q, CELLS, Sh::JS>(Kc, cf, c < nt, q, sW, sD, sP, pp + Sh::QSOFF, pp,
+                                             pp + Sh::GOFF);
+        } else if (q < Q && !(PAIR_ABL & 4)) {
           double* qsp = rec + Sh::QS * NS * Sh::JS + ql * Sh::QSD * CELLS + c;
           double* rp = rec + ql * NS * Sh::JS + c;
           const double* Kc = cell + c * Sh::CELLD;
