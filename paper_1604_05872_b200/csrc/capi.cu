@@ -383,7 +383,7 @@ Peaks device_peaks() {
 // profiles/schedule_choice_r02.json, tools/sched_compare.py).  The quadrature
 // Helmholtz kernel maps one warp per 4x4 (j,k) tile: ns = 4 keeps one of 16 warps busy.
 constexpr double kEffHelmP1 = 0.831, kEffHelmTensor = 0.754, kEffPairElas = 0.726,
-                 kEffElasTensor = 0.381, kEffPairSvk = 0.505, kEffBurgers = 0.589,
+                 kEffElasTensor = 0.381, kEffPairSvk = 0.524, kEffBurgers = 0.589,
                  kEffSvkMma = 0.458;
 double eff_helm_quad(int ns) { return ns >= 20 ? 0.245 : ns >= 10 ? 0.2 : 0.04; }
 
