@@ -233,7 +233,8 @@ def f_alg(cfg_name):
 
 
 KERNEL_SOURCES = {"helm_quad": "helm_quad.cu", "helm_": "helmholtz.cu", "pair_": "pair.cu",
-                  "burgers": "burgers.cu", "elas_": "elasticity.cu", "svk_mma": "svk_mma.cu"}
+                  "burgers_quad": "burgers_quad.cu", "burgers": "burgers.cu", "elas_": "elasticity.cu",
+                  "svk_mma": "svk_mma.cu"}
 
 
 def kernel_source_sha(kernel_name: str):

@@ -64,7 +64,8 @@ enum Route {
   ROUTE_PAIR,
   ROUTE_ELAS_TENSOR,
   ROUTE_BURGERS,
-  ROUTE_SVK_MMA
+  ROUTE_SVK_MMA,
+  ROUTE_BURGERS_QUAD
 };
 
 std::string two(int m) {
@@ -384,7 +385,7 @@ Peaks device_peaks() {
 // Helmholtz kernel maps one warp per 4x4 (j,k) tile: ns = 4 keeps one of 16 warps busy.
 constexpr double kEffHelmP1 = 0.831, kEffHelmTensor = 0.754, kEffPairElas = 0.726,
                  kEffElasTensor = 0.381, kEffPairSvk = 0.524, kEffBurgers = 0.589,
-                 kEffSvkMma = 0.458;
+                 kEffSvkMma = 0.458, kEffBurgersQuad = 0.236;
 double eff_helm_quad(int ns) { return ns >= 20 ? 0.245 : ns >= 10 ? 0.2 : 0.04; }
 
 std::vector<Cand> candidates(const femgpu_form_desc* d) {
@@ -446,6 +447,12 @@ std::vector<Cand> candidates(const femgpu_form_desc* d) {
                          60 * 7 + 60,
                      kEffBurgers, "burgers_kernel"});
       }
+      if (femgpu::burgers_quad_supported(Q, ns))
+        // per point: u, grad u (420 FMA, once per cell); per (j, k): g_k (9, per lane
+        // and j group), the nine d_d u_c sums (9) and the scalar term (~6)
+        c.push_back({ROUTE_BURGERS_QUAD, FEMGPU_SCHED_QUADRATURE, 0,
+                     2.0 * Q * (420 + ns / 4 * ns * 12 + (double)ns * ns * 16), kEffBurgersQuad,
+                     "burgers_quad_kernel"});
       break;
   }
   return c;
@@ -506,6 +513,10 @@ void launch(const femgpu_form* f, long E, const double* coords, const double* co
       break;
     case ROUTE_SVK_MMA:
       e = femgpu::launch_svk_mma(f->nq, f->ns, E, coords, coef, f->d_tab, A, acc, s);
+      break;
+    case ROUTE_BURGERS_QUAD:
+      e = femgpu::launch_burgers_quad(f->nq, f->ns, E, coords, coef, f->d_tab, f->consts[0],
+                                      f->consts[1], A, acc, s);
       break;
     case ROUTE_BURGERS:
       e = femgpu::launch_burgers(f->ns, E, coords, coef, f->d_tab, f->consts[0], f->consts[1], A,
@@ -578,6 +589,11 @@ int femgpu_form_create(const femgpu_form_desc* d, femgpu_form** out) {
         break;
       case ROUTE_HELM_TENSOR:
         build_helm_tensor(f.get(), host);
+        break;
+      case ROUTE_BURGERS_QUAD:  // W | B | D
+        host.insert(host.end(), f->W.begin(), f->W.end());
+        host.insert(host.end(), f->B.begin(), f->B.end());
+        host.insert(host.end(), f->D.begin(), f->D.end());
         break;
       case ROUTE_HELM_QUAD:  // W | B | D | P
         host.insert(host.end(), f->W.begin(), f->W.end());

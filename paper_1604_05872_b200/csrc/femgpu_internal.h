@@ -59,6 +59,13 @@ bool svk_mma_supported(int nq, int ns);
 cudaError_t launch_svk_mma(int nq, int ns, long E, const double* coords, const double* coef,
                            const double* tab, double* A, int acc, cudaStream_t s);
 
+// Burgers Jacobian in the quadrature schedule (see burgers_quad.cu).
+// tab = [W(Q) | B(Q,ns) | D(3,Q,ns)].
+bool burgers_quad_supported(int nq, int ns);
+cudaError_t launch_burgers_quad(int nq, int ns, long E, const double* coords, const double* coef,
+                                const double* tab, double nu, double dt, double* A, int acc,
+                                cudaStream_t s);
+
 // Linear elasticity tensor schedule (see elasticity.cu).
 bool elas_tensor_supported(int ns, int nc);
 size_t elas_tensor_table_doubles();

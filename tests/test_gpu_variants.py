@@ -104,6 +104,31 @@ def test_svk_tensor_core_quadrature(name):
         assert frob_rel(out.cpu().numpy() - 1.5, R) < 1e-11, E
 
 
+def test_burgers_quadrature_schedule():
+    # the Burgers Jacobian in the quadrature schedule (burgers_quad.cu), on request:
+    # several passes of the persistent grid (E > 148 x 12), ragged sizes, accumulate
+    import port
+
+    cfg = fe.CONFIGS["c5"]
+    tabs = fe.tables(cfg)
+    form = femgpu.Form.from_config(cfg, tabs, schedule=femgpu.SCHED_QUADRATURE)
+    assert form.info["kernel_name"] == "burgers_quad_kernel"
+    dev = torch.device("cuda:0")
+    for E in (1, 13, 2 * 148 * 12 + 7):
+        coords, coeffs = fe.cell_inputs(cfg, ncells=E)
+        R = port.assemble(cfg, tabs, coords, coeffs)
+        x = torch.from_numpy(coords).to(dev)
+        c = torch.from_numpy(coeffs).to(dev)
+        out = torch.empty((E, cfg.n, cfg.n), dtype=torch.float64, device=dev)
+        form.assemble(x, c, out)
+        torch.cuda.synchronize()
+        assert frob_rel(out.cpu().numpy(), R) < TOL, E
+        out.fill_(1.5)
+        form.assemble(x, c, out, accumulate=True)
+        torch.cuda.synchronize()
+        assert frob_rel(out.cpu().numpy() - 1.5, R) < 1e-11, E
+
+
 def test_schedule_contract():
     # Helmholtz and elasticity have both schedules (AUTO: tensor resp. quadrature,
     # the faster ones, tests/test_schedule.py); St Venant-Kirchhoff only quadrature

@@ -118,7 +118,7 @@ def test_quadrature_kernel_ragged_and_accumulate():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
 def test_auto_choice_is_the_faster_measured(name):
     """On the BASELINE mesh, the kernel AUTO picks runs faster than the other
     schedule's kernel (timed with CUDA events over a CUDA-graph replay)."""
