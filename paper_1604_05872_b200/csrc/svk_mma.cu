@@ -182,24 +182,24 @@ __global__ void __launch_bounds__(SvkMmaShape<Q>::THREADS, SvkMmaShape<Q>::CTAS_
         const int nks = min(Sh::KSPS, (Q - st * Sh::QS + 3) / 4);
 #pragma unroll 1
         for (int ks = 0; ks < nks; ++ks) {
-        const double* sg = sRing + b * Sh::STAGE_DBL + w * Sh::CS + ks * Sh::KB;
-        const double lam = sg[Sh::OLM + 2 * qi], mu = sg[Sh::OLM + 2 * qi + 1];
-        double x[4];
+          const double* sg = sRing + b * Sh::STAGE_DBL + w * Sh::CS + ks * Sh::KB;
+          const double lam = sg[Sh::OLM + 2 * qi], mu = sg[Sh::OLM + 2 * qi + 1];
+          double x[4];
 #pragma unroll
-        for (int m = 0; m < 4; ++m) x[m] = sg[Sh::OX + 32 * m + lane];
-        const double mf = sg[Sh::OM + lane];
-        if (!(SVKM_ABL & 1)) {
+          for (int m = 0; m < 4; ++m) x[m] = sg[Sh::OX + 32 * m + lane];
+          const double mf = sg[Sh::OM + lane];
+          if (!(SVKM_ABL & 1)) {
 #pragma unroll
-        for (int t = 0; t < Sh::NPT; ++t) dmma8x8x4(wc[t], mf, sg[Sh::OG + 32 * t + lane]);
+            for (int t = 0; t < Sh::NPT; ++t) dmma8x8x4(wc[t], mf, sg[Sh::OG + 32 * t + lane]);
 #pragma unroll
-        for (int t = 0; t < Sh::NYT; ++t) {
-          dmma8x8x4(yl[t], lam * x[ytile_m(t)], x[ytile_n(t)]);
-          dmma8x8x4(ym[t], mu * x[ytile_m(t)], x[ytile_n(t)]);
-        }
-        } else {  // keep the loads alive
-          yl[0][0] += lam * x[0] + mf + x[1] + x[2] + x[3];
-          ym[0][0] += mu;
-        }
+            for (int t = 0; t < Sh::NYT; ++t) {
+              dmma8x8x4(yl[t], lam * x[ytile_m(t)], x[ytile_n(t)]);
+              dmma8x8x4(ym[t], mu * x[ytile_m(t)], x[ytile_n(t)]);
+            }
+          } else {  // ablation: keep the loads alive
+            yl[0][0] += lam * x[0] + mf + x[1] + x[2] + x[3];
+            ym[0][0] += mu;
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[b]);
