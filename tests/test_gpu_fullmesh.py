@@ -37,9 +37,9 @@ MULTI_TILE = {"c1": 3 * 444 * 256 + 77, "c2": 3 * 148 * 32 + 97, "c3": 3 * 296 *
               "c4": 3 * 148 * 16 + 13, "c5": 3 * 148 * 16 + 13}
 
 
-def _device_launch(cfg, coords, coeffs):
+def _device_launch(cfg, coords, coeffs, schedule=femgpu.SCHED_AUTO):
     dev = torch.device("cuda:0")
-    form = femgpu.Form.from_config(cfg)
+    form = femgpu.Form.from_config(cfg, schedule=schedule)
     x = torch.from_numpy(coords).to(dev)
     c = torch.from_numpy(coeffs).to(dev)
     out = torch.full((coords.shape[0], cfg.n, cfg.n), float("nan"), dtype=torch.float64,
@@ -56,6 +56,27 @@ def test_full_mesh_every_cell_vs_reference(name):
     cfg = fe.CONFIGS[name]
     coords, coeffs = fe.cell_inputs(cfg)
     _, out = _device_launch(cfg, coords, coeffs)
+    r = parity.check(cfg, coords, coeffs, lambda a, b: out[a:b].cpu().numpy())
+    assert r["cells_checked"] == cfg.ncells
+    assert r["max_frob_rel"] < TOL, r
+
+
+# the second schedule of each family, on the same full meshes (the cost model
+# ranks them behind AUTO's choice; profiles/schedule_choice_r02.json)
+ALTERNATIVES = [("c2", femgpu.SCHED_QUADRATURE, "helm_quad_kernel"),
+                ("c3", femgpu.SCHED_TENSOR, "elas_tensor_kernel"),
+                ("c4", femgpu.SCHED_QUADRATURE_MMA, "svk_mma_kernel"),
+                ("c5", femgpu.SCHED_QUADRATURE, "burgers_quad_kernel")]
+
+
+@pytest.mark.parametrize("name,schedule,kernel", ALTERNATIVES)
+def test_full_mesh_alternative_schedules_vs_reference(name, schedule, kernel):
+    import parity
+
+    cfg = fe.CONFIGS[name]
+    coords, coeffs = fe.cell_inputs(cfg)
+    form, out = _device_launch(cfg, coords, coeffs, schedule)
+    assert form.info["kernel_name"] == kernel
     r = parity.check(cfg, coords, coeffs, lambda a, b: out[a:b].cpu().numpy())
     assert r["cells_checked"] == cfg.ncells
     assert r["max_frob_rel"] < TOL, r
