@@ -85,6 +85,9 @@
 #ifndef PAIR_SVK_PW
 #define PAIR_SVK_PW 3  // SVK ws: producer warps that build ring stages (of 4)
 #endif
+#ifndef PAIR_SVK_QUNROLL
+#define PAIR_SVK_QUNROLL 2  // SVK ws consumers: unroll of a stage's points (1: 1.147 vs 1.107 ms)
+#endif
 #ifndef PAIR_SVK_GREC
 #define PAIR_SVK_GREC 1  // SVK ws: records h_j + G_jk (producers do the g_j.g_k) instead of g_j | h_j
 #endif
@@ -102,6 +105,7 @@ namespace femgpu {
 
 constexpr int kPairQUnroll = PAIR_QUNROLL;
 constexpr int kPairWsQUnroll = PAIR_WS_QUNROLL;
+constexpr int kSvkQUnroll = PAIR_SVK_QUNROLL;
 
 template <int KIND, int NS, int Q>
 struct PairShape {
@@ -1189,7 +1193,7 @@ __global__ void __launch_bounds__(SvkWsShape<NS, Q>::THREADS, SvkWsShape<NS, Q>:
           if (sl.active && !(PAIR_ABL & 1)) {
             if (dwarp) {
               if (nq == Sh::QS) {
-#pragma unroll
+#pragma unroll kSvkQUnroll
                 for (int ql = 0; ql < Sh::QS; ++ql)
                   svk_point_g_diag<Sh>(a4, t1, pt + ql * Sh::PT_DBL, pt + ql * Sh::PT_DBL + Sh::GOFF,
                                        pt + ql * Sh::PT_DBL + Sh::QSOFF, sl.j0, pidx);
@@ -1200,7 +1204,7 @@ __global__ void __launch_bounds__(SvkWsShape<NS, Q>::THREADS, SvkWsShape<NS, Q>:
               }
             } else {
               if (nq == Sh::QS) {
-#pragma unroll
+#pragma unroll kSvkQUnroll
                 for (int ql = 0; ql < Sh::QS; ++ql)
                   svk_point_g<Sh>(a4, t1, pt + ql * Sh::PT_DBL, pt + ql * Sh::PT_DBL + Sh::GOFF,
                                   pt + ql * Sh::PT_DBL + Sh::QSOFF, sl.j0, sl.k0, pidx);
