@@ -39,13 +39,14 @@
 //  * pair_ws_kernel  (elasticity): warp-specialised -- 2 producer warps build
 //    the records of the next tile into a double buffer (mbarrier full/empty)
 //    while 4 consumer warps accumulate; 2 CTAs per SM;
-//  * pair_svk_ws_kernel (SVK): warp-specialised with a deeper ring -- 4 producer
-//    warps run the heavier per-point setup (F, tr E, F F^T, 10 records per (cell, q))
-//    into a 5-slot ring of 2-point stages while 8 consumer warps (2 cells each)
-//    accumulate; one CTA of 16 cells per SM pools the shared memory for the ring;
+//  * pair_svk_ws_kernel (SVK): warp-specialised with a deeper ring -- 3 producer
+//    warps run the heavier per-point setup (F, tr E, F F^T, h_j, G_jk per (cell, q))
+//    into a 4-slot ring of 2-point stages while 8 consumer warps (off-diagonal and
+//    diagonal tiles in warps of their own) accumulate; one CTA of 16 cells per SM
+//    pools the shared memory for the ring (c4: 1.107 ms);
 //  * pair_flat_kernel (SVK before, PAIR_SVK_WS=0): every thread takes part in each
 //    phase; 2 CTAs per SM overlap one CTA's setup with the other's FMA stream
-//    (c4 1.31 ms against 1.25 ms for the ring kernel).
+//    (c4 1.31 ms against 1.25 ms for the round-1 ring kernel).
 //
 // SVK accumulates each 3x3 (c,d) block as its symmetric and antisymmetric parts
 // (pair_point, svk_unfold): 27 instead of 33 FP64 instructions per pair and point.
@@ -1037,9 +1038,13 @@ struct SvkTables {
 // warp's two (j,k) tiles are warp-uniform, so the 10 off-diagonal 2x2 tiles fill 5
 // warps and the 5 diagonal ones -- whose k side is their j side (pair_point_diag:
 // 20 instead of 32 loads, 87 instead of 126 FP64 instructions per point) -- 3 warps.
-// The tile's 16 cells are staged together and bulk-stored two per warp.  Of the 4
-// producer warps the first only loads inputs and computes the geometry, keeping the
-// sub-partition with two off-diagonal consumer warps free of setup work.
+// With G records (PAIR_SVK_GREC) the producers store h_j and G_jk = g_j.g_k per point
+// and the consumers read 24 (diagonal tiles 17) operands per point.  The tile's 16
+// cells are staged together: each consumer warp stages its tiles and arrives on an
+// mbarrier; one issuer bulk-stores the 16 cells and releases the staging halfway
+// through the next tile, so no consumer waits for another at the tile end.  Of the
+// 4 producer warps the first only loads inputs and computes the geometry, keeping
+// the sub-partition with two off-diagonal consumer warps free of setup work.
 // ============================================================================
 template <int NS_, int Q>
 struct SvkWsShape {
