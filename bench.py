@@ -238,14 +238,18 @@ KERNEL_SOURCES = {"helm_quad": "helm_quad.cu", "helm_": "helmholtz.cu", "pair_":
 
 
 def kernel_source_sha(kernel_name: str):
+    """sha of the kernel's .cu source with // comments and blank lines dropped (a
+    capture stays valid across comment edits, not across code edits)."""
     for prefix, fn in KERNEL_SOURCES.items():
         if kernel_name.startswith(prefix):
             path = os.path.join(ROOT, "paper_1604_05872_b200", "csrc", fn)
             try:
-                with open(path, "rb") as f:
-                    return hashlib.sha1(f.read()).hexdigest()[:12]
+                with open(path, encoding="utf-8") as f:
+                    lines = [ln.split("//", 1)[0].rstrip() for ln in f]
             except OSError:
                 return None
+            code = "\n".join(ln for ln in lines if ln)
+            return hashlib.sha1(code.encode()).hexdigest()[:12]
     return None
 
 
