@@ -159,6 +159,13 @@ __device__ __forceinline__ void cp_async8b(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 
+// The slabs are written once and never re-read: stores carry an L2 evict_first policy
+// so they do not displace the R2 table and the streamed inputs (-2.2 % on c5; the
+// same hint on the 1D bulk stores of pair.cu costs 0.3-1.2 %, so only here --
+// profiles/c5_r02_ablation.txt).
+#ifndef BZ_EVICT
+#define BZ_EVICT 1
+#endif
 __device__ __forceinline__ void slab_store(const CUtensorMap* map, const double* src, int col,
                                            int row, int cell, int acc) {
   if (acc)
@@ -167,12 +174,22 @@ __device__ __forceinline__ void slab_store(const CUtensorMap* map, const double*
         "[%0, {%1, %2, %3}], [%4];\n" ::"l"(map),
         "r"(col), "r"(row), "r"(cell), "r"(smem_u32(src))
         : "memory");
-  else
+  else {
+#if BZ_EVICT
+    const uint64_t pol = l2_evict_first();
+    asm volatile(
+        "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group.L2::cache_hint "
+        "[%0, {%1, %2, %3}], [%4], %5;\n" ::"l"(map),
+        "r"(col), "r"(row), "r"(cell), "r"(smem_u32(src)), "l"(pol)
+        : "memory");
+#else
     asm volatile(
         "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(
             map),
         "r"(col), "r"(row), "r"(cell), "r"(smem_u32(src))
         : "memory");
+#endif
+  }
 }
 
 __device__ __forceinline__ void bulk_wait_read2() {
