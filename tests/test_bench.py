@@ -86,3 +86,28 @@ def test_config_dict_and_args():
     w = bench.config_dict(fe.CONFIGS["c5"], 8, "weak")
     assert s["cells"] == fe.CONFIGS["c5"].ncells and w["cells"] == 8 * fe.CONFIGS["c5"].ncells
     assert "contiguously over 8" in s["parallelism"]
+
+
+def test_committed_ncu_captures_match_kernel_sources():
+    """Every config's committed ncu capture (profiles/ncu_summary.json) belongs to the
+    current source of its kernel, so the bench's roofline uses the ncu-counted F_exec
+    and DRAM traffic instead of falling back to the flop model."""
+    with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+        summ = json.load(f)
+    for cfg in bench.CONFIG_ORDER:
+        d = summ[cfg]
+        name = d["kernel"].split("(")[0].split("<")[0].replace("void ", "").split("::")[-1]
+        assert bench.kernel_source_sha(name) == d["src_sha"], (cfg, name)
+        assert bench.ncu_capture(cfg, name) is not None, cfg
+
+
+def test_kernel_source_sha_ignores_comments(tmp_path, monkeypatch):
+    src = tmp_path / "paper_1604_05872_b200" / "csrc"
+    src.mkdir(parents=True)
+    (src / "pair.cu").write_text("int f() {\n  return 1;  // one\n}\n")
+    monkeypatch.setattr(bench, "ROOT", str(tmp_path))
+    a = bench.kernel_source_sha("pair_ws_kernel")
+    (src / "pair.cu").write_text("// header\n\nint f() {\n  return 1;  // uno\n}\n")
+    assert bench.kernel_source_sha("pair_ws_kernel") == a
+    (src / "pair.cu").write_text("int f() {\n  return 2;\n}\n")
+    assert bench.kernel_source_sha("pair_ws_kernel") != a
